@@ -1,0 +1,192 @@
+/*
+ * fea_gpu.h — C ABI of the B200-native FE assembly hot path
+ * (scatter-add of dense element matrices into CSR / CRAC, arXiv 2012.00585).
+ *
+ * The reference (/root/reference/proj) exposes this path only as C++ templates
+ * (no C ABI). Each entry point below names the reference interface it replaces;
+ * the C++ shim paper_2012_00585_b200/csrc/fea_gpu.hpp re-exposes the reference
+ * surface (SparsityPattern, CsrMatrix, CracMatrix, AssemblyJob, assemble_*,
+ * AssemblyError) on top of it, and INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - index_t is int64_t everywhere, as in the reference (types.hpp:27).
+ *  - Element DOF arrays are the reference's ElementDofs::flat
+ *    (dof_map.hpp:66-75) for all elements, concatenated: E x m int64,
+ *    host or device memory (detected).
+ *  - Element matrices K are one dense buffer [E][m][m] fp64 row-major in DEVICE
+ *    memory (the reference's ElementMatrix, dof_map.hpp:78-87, materialized for
+ *    every element instead of an ElementMatrixSupplier callback,
+ *    assembly.hpp:37).
+ *  - values is a caller-owned fp64[nnz] buffer. CSR and CRAC store values in the
+ *    same order (row-major, ascending columns; verify.cpp:30-31), so one
+ *    numeric call serves both formats.
+ *  - Calls are stream-ordered on the given cudaStream_t (NULL = legacy default
+ *    stream); a plan is bound to one device and is not thread-safe.
+ *  - Every function returns fea_status; fea_last_error() holds the message of
+ *    the last failure on the calling thread.
+ */
+#ifndef FEA_GPU_H
+#define FEA_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FEA_OK = 0,
+    FEA_ERR_INVALID = 1,        /* std::invalid_argument / std::out_of_range (dof_map.cpp:25-27, :82-84) */
+    FEA_ERR_MISSING_ENTRY = 2,  /* AssemblyError, assembly.hpp:65-73 */
+    FEA_ERR_OOM = 3,            /* std::bad_alloc (bench.cpp:257-264) */
+    FEA_ERR_CUDA = 4,
+    FEA_ERR_INVALID_COLOURING = 5 /* AssemblyError("invalid colouring: ...") assembly.hpp:178-182 */
+} fea_status;
+
+/* Conflict strategies of the numeric phase. */
+typedef enum {
+    /* fp64 atomicAdd per entry — the GPU form of assemble_atomic
+     * (assembly.hpp:121-126, AtomicValues formats.hpp:123-138). Matches
+     * assemble_sequential within |a-b| <= 1e-12*max(|a|,|b|,1). */
+    FEA_ATOMIC = 0,
+    /* Deterministic sort-by-slot segmented reduction: every value slot is a
+     * left fold, starting from the slot's value, over its contributions in
+     * ascending element id — bit-identical to assemble_sequential
+     * (assembly.hpp:112-118). */
+    FEA_DET_SORTED = 1,
+    /* Deterministic colouring route: one pass per colour, plain adds — the GPU
+     * form of assemble_coloured_vectorized (assembly.hpp:175-195); bit-identical
+     * to it under the same colouring. Needs fea_plan_set_colouring(). */
+    FEA_DET_COLOUR = 2
+} fea_strategy;
+
+/* fea_assemble flags */
+#define FEA_ACCUMULATE 0u /* values += assembled (reference semantics: assemble adds) */
+#define FEA_OVERWRITE 1u  /* values  = assembled (== reset_values, formats.hpp:351-354, then assemble) */
+
+/* fea_plan_create flags */
+#define FEA_PLAN_K_COMPACT 1u /* K holds only the plan's kept elements, in ascending element id
+                                 (row-partitioned plans); default: K holds all E elements */
+
+/* fea_plan_create_with_pattern formats */
+#define FEA_FORMAT_CSR 0
+#define FEA_FORMAT_CRAC 1
+
+typedef struct fea_plan fea_plan;
+
+/* Message of the last failure on this thread ("" if none). */
+const char* fea_last_error(void);
+
+/* Library/ABI version: major*10000 + minor*100 + patch. */
+int fea_version(void);
+
+/*
+ * Symbolic phase + slot-map build.
+ * Replaces: fea::build_pattern(const DofMap&) (pattern.hpp:40, pattern.cpp:24-108)
+ *           + CsrMatrix(pattern) / CracMatrix(pattern) (formats.hpp:157-160, :268-273,
+ *             build_crac_arrays formats.cpp:21-41)
+ *           + the per-entry locate() of scatter_element (assembly.hpp:84), resolved once.
+ *  elem_dofs     E x m int64 DOFs (ElementDofs::flat of every element), host or device
+ *  n_rows        number of global rows (DofMap::n_dofs)
+ *  dofs_per_node d of the DofMap (dof(v,k) = v*d+k, dof_map.hpp:59); the plan verifies
+ *                the node-contiguous layout and falls back to d = 1 if it does not hold
+ *  row_begin/end owned global row range [row_begin, row_end) (multiples of d); the
+ *                whole matrix is [0, n_rows). Only owned rows are assembled; the
+ *                plan's CSR/CRAC row block is rebased to 0, columns stay global.
+ */
+fea_status fea_plan_create(int device, const int64_t* elem_dofs, int64_t n_elements, int32_t m,
+                           int64_t n_rows, int32_t dofs_per_node, int64_t row_begin,
+                           int64_t row_end, uint32_t flags, fea_plan** out);
+
+/*
+ * Plan against an externally supplied pattern (whole matrix).
+ * Replaces: CsrMatrix(const SparsityPattern&) / CracMatrix(...) built from a
+ * caller's pattern (formats.hpp:157, :268) + the locate() of every element entry:
+ * CSR lower-bound search (formats.hpp:165-199) or CRAC Listing-1 block search
+ * (formats.hpp:276-290), warp-cooperative on the device. An element entry absent
+ * from the pattern is recorded (lowest element id) and makes fea_assemble fail
+ * with FEA_ERR_MISSING_ENTRY, as scatter_element throws (assembly.hpp:85-87).
+ *  format FEA_FORMAT_CSR : row_ptr[n_rows+1], idx = cols[nnz]
+ *  format FEA_FORMAT_CRAC: row_ptr[n_rows+1] in col_align entry units, idx = col_align[2*runs+2]
+ */
+fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, int64_t n_elements,
+                                        int32_t m, int64_t n_rows, int32_t format,
+                                        const int64_t* row_ptr, const int64_t* idx,
+                                        fea_plan** out);
+
+void fea_plan_destroy(fea_plan* plan);
+
+/* Sizes of the plan's (owned) row block: rows, nnz (= values length), CRAC runs
+ * (count_pattern_runs, pattern.cpp:110-120), kept elements. */
+fea_status fea_plan_sizes(const fea_plan* plan, int64_t* n_rows, int64_t* nnz, int64_t* n_runs,
+                          int64_t* n_elements);
+
+/* Slot-map / plan details for reporting: dofs per node used, nodes per element,
+ * bytes of device metadata held by the plan. */
+fea_status fea_plan_info(const fea_plan* plan, int32_t* dofs_per_node, int32_t* nodes_per_element,
+                         int64_t* metadata_bytes);
+
+/* CSR arrays of the plan (SparsityPattern::row_ptr/cols, pattern.hpp:29-35):
+ * row_ptr[n_rows+1], cols[nnz]; host or device destinations. */
+fea_status fea_plan_copy_csr(const fea_plan* plan, int64_t* row_ptr, int64_t* cols);
+
+/* CRAC arrays (CracBase::rows / col_align, formats.hpp:257-273): row_ptr[n_rows+1]
+ * in col_align entry units, col_align[2*runs+2] with the final (0, nnz) pair. */
+fea_status fea_plan_copy_crac(const fea_plan* plan, int64_t* row_ptr, int64_t* col_align);
+
+/* Ids (ascending) of the elements the plan keeps (those with a node in the owned
+ * row range); elem_ids[n_elements] from fea_plan_sizes. */
+fea_status fea_plan_copy_elements(const fea_plan* plan, int64_t* elem_ids);
+
+/* Greedy colouring of the plan's elements — fea::greedy_colouring
+ * (colouring.cpp:24-75): ascending element order, smallest colour unused by any
+ * node-sharing element. colour_of[E] (host). */
+fea_status fea_plan_greedy_colouring(const fea_plan* plan, int32_t* colour_of, int32_t* n_colours);
+
+/* Install the colouring used by FEA_DET_COLOUR (Colouring::colour_of,
+ * colouring.hpp:35-39; host array over all E input elements). Validated like
+ * find_colour_conflict (colouring.cpp:91-119): two same-colour elements sharing
+ * a DOF -> FEA_ERR_INVALID_COLOURING. */
+fea_status fea_plan_set_colouring(fea_plan* plan, const int32_t* colour_of);
+
+/*
+ * Numeric phase.
+ * Replaces: assemble_atomic / assemble_sequential / assemble_coloured_vectorized
+ * (assembly.hpp:112-195) on CsrMatrix / CsrAtomicMatrix / CracMatrix /
+ * CracAtomicMatrix targets.
+ *  K       device [E][m][m] fp64 (or [kept][m][m] with FEA_PLAN_K_COMPACT)
+ *  values  device fp64[nnz]
+ *  flags   FEA_ACCUMULATE or FEA_OVERWRITE
+ *  stream  cudaStream_t (as void*)
+ */
+fea_status fea_assemble(fea_plan* plan, const double* K, int32_t strategy, double* values,
+                        uint32_t flags, void* stream);
+
+/* End-to-end form with HOST buffers (pinned or pageable): copies K host->device,
+ * assembles, copies values device->host; synchronous like the reference call
+ * (SPEC.md:364). Device staging buffers are cached in the plan. */
+fea_status fea_assemble_host(fea_plan* plan, const double* K_host, int32_t strategy,
+                             double* values_host, uint32_t flags, void* stream);
+
+/* The missing entry behind FEA_ERR_MISSING_ENTRY: element, row, column (the
+ * values AssemblyError names, assembly.hpp:65-73). Returns FEA_OK with e = -1
+ * when the plan has none. */
+fea_status fea_plan_missing_entry(const fea_plan* plan, int64_t* element, int64_t* row,
+                                  int64_t* col);
+
+/* Number of kernel launches the last fea_assemble issued on this plan. */
+int32_t fea_plan_last_launches(const fea_plan* plan);
+
+/* Seeded synthetic element matrices: K[i][r][c] = U(seed, id_i, min(r,c), max(r,c)),
+ * symmetric, uniform on [-1,1), exactly representable (the counter-hash supplier of
+ * SURVEY.md §7.2; stands in for ElementMatrixSupplier, assembly.hpp:37).
+ * elem_ids: NULL (id_i = i) or device int64[n]. */
+fea_status fea_fill_seeded_k(double* K, int64_t n, int32_t m, uint64_t seed,
+                             const int64_t* elem_ids, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FEA_GPU_H */

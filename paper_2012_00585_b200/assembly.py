@@ -1,0 +1,214 @@
+"""Python host interface over the C ABI (used by bench.py and the tests).
+
+Mirrors the reference's assembly surface (proj/include/fea/*.hpp):
+  * ``Plan``                    — SparsityPattern + CsrMatrix/CracMatrix construction
+                                  (build_pattern pattern.cpp:24-108, formats.hpp:157/:268) and the
+                                  cached slot map; one plan serves CSR and CRAC (same values order,
+                                  verify.cpp:30-31)
+  * ``Plan.assemble(K, ...)``   — assemble_atomic / assemble_sequential /
+                                  assemble_coloured_vectorized (assembly.hpp:112-195)
+  * ``AssemblyError``           — fea::AssemblyError (types.hpp:31-33): missing entry, bad colouring
+Device memory and streams come from torch; torch types never cross the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes
+from ctypes import byref, c_int32, c_int64, c_void_p
+
+import numpy as np
+
+from . import _native as N
+
+STRATEGIES = {"atomic": N.FEA_ATOMIC, "sorted": N.FEA_DET_SORTED, "colour": N.FEA_DET_COLOUR}
+
+
+class FeaError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(message)
+        self.status = status
+
+
+class AssemblyError(FeaError):
+    """fea::AssemblyError: coefficient missing from the pattern, or invalid colouring."""
+
+
+def _check(status: int) -> None:
+    if status == N.FEA_OK:
+        return
+    msg = N.last_error()
+    if status in (N.FEA_ERR_MISSING_ENTRY, N.FEA_ERR_INVALID_COLOURING):
+        raise AssemblyError(status, msg)
+    if status == N.FEA_ERR_OOM:
+        raise MemoryError(msg)
+    if status == N.FEA_ERR_INVALID:
+        raise ValueError(msg)
+    raise FeaError(status, msg)
+
+
+def _ptr(x) -> c_void_p:
+    """Raw pointer of a numpy array or torch tensor (contiguous)."""
+    if x is None:
+        return c_void_p(0)
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"]
+        return c_void_p(x.ctypes.data)
+    assert x.is_contiguous()
+    return c_void_p(x.data_ptr())
+
+
+def _stream_ptr(stream) -> c_void_p:
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return c_void_p(stream.cuda_stream)
+
+
+def _as_int64_dofs(elem_dofs):
+    if isinstance(elem_dofs, np.ndarray):
+        a = np.ascontiguousarray(elem_dofs, dtype=np.int64)
+        return a, a.shape[0] if a.ndim == 2 else 0, a.shape[1] if a.ndim == 2 else 0
+    import torch
+    t = elem_dofs.to(torch.int64).contiguous()
+    return t, t.shape[0], t.shape[1]
+
+
+class Plan:
+    """Symbolic phase + slot map on one GPU for E elements with m DOFs each.
+
+    elem_dofs : (E, m) int64 — ElementDofs::flat of every element (host numpy or torch tensor)
+    n_rows    : global number of rows (DofMap::n_dofs)
+    dofs_per_node : d (DOFs v*d..v*d+d-1 per node, dof_map.hpp:59); detected, 1 if absent
+    row_range : owned [row_begin, row_end) for row-partitioned assembly (default: all rows)
+    k_compact : K holds only the kept elements (ascending id) instead of all E
+    """
+
+    def __init__(self, elem_dofs, n_rows: int, dofs_per_node: int = 1, row_range=None,
+                 device: int = 0, k_compact: bool = False, _handle=None):
+        self._lib = N.lib()
+        self.device = device
+        self._h = c_void_p(0)
+        if _handle is not None:
+            self._h = _handle
+        else:
+            dofs, E, m = _as_int64_dofs(elem_dofs)
+            rb, re = (0, n_rows) if row_range is None else row_range
+            flags = N.FEA_PLAN_K_COMPACT if k_compact else 0
+            h = c_void_p(0)
+            _check(self._lib.fea_plan_create(device, _ptr(dofs), E, m, n_rows, dofs_per_node, rb, re,
+                                             flags, byref(h)))
+            self._h = h
+        self._refresh()
+
+    @classmethod
+    def with_pattern(cls, elem_dofs, n_rows: int, row_ptr, idx, fmt: str = "csr", device: int = 0):
+        """Plan against a caller-supplied CSR (row_ptr, cols) or CRAC (row_ptr, col_align) pattern."""
+        lib = N.lib()
+        dofs, E, m = _as_int64_dofs(elem_dofs)
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ix = np.ascontiguousarray(idx, dtype=np.int64)
+        f = N.FEA_FORMAT_CSR if fmt == "csr" else N.FEA_FORMAT_CRAC
+        h = c_void_p(0)
+        _check(lib.fea_plan_create_with_pattern(device, _ptr(dofs), E, m, n_rows, f, _ptr(rp),
+                                                _ptr(ix), byref(h)))
+        return cls(None, n_rows, device=device, _handle=h)
+
+    def _refresh(self):
+        r, z, u, e = c_int64(), c_int64(), c_int64(), c_int64()
+        _check(self._lib.fea_plan_sizes(self._h, byref(r), byref(z), byref(u), byref(e)))
+        self.n_rows, self.nnz, self.n_runs, self.n_elements = r.value, z.value, u.value, e.value
+        d, npe, meta = c_int32(), c_int32(), c_int64()
+        _check(self._lib.fea_plan_info(self._h, byref(d), byref(npe), byref(meta)))
+        self.dofs_per_node, self.nodes_per_element, self.metadata_bytes = d.value, npe.value, meta.value
+
+    # -- symbolic outputs -------------------------------------------------
+    def csr(self):
+        row_ptr = np.empty(self.n_rows + 1, np.int64)
+        cols = np.empty(max(self.nnz, 1), np.int64)
+        _check(self._lib.fea_plan_copy_csr(self._h, _ptr(row_ptr), _ptr(cols)))
+        return row_ptr, cols[: self.nnz]
+
+    def crac(self):
+        row_ptr = np.empty(self.n_rows + 1, np.int64)
+        col_align = np.empty(2 * self.n_runs + 2, np.int64)
+        _check(self._lib.fea_plan_copy_crac(self._h, _ptr(row_ptr), _ptr(col_align)))
+        return row_ptr, col_align
+
+    def elements(self):
+        out = np.empty(max(self.n_elements, 1), np.int64)
+        _check(self._lib.fea_plan_copy_elements(self._h, _ptr(out)))
+        return out[: self.n_elements]
+
+    def greedy_colouring(self):
+        col = np.empty(max(self.n_elements, 1), np.int32)
+        nc = c_int32()
+        _check(self._lib.fea_plan_greedy_colouring(self._h, _ptr(col), byref(nc)))
+        return col[: self.n_elements], nc.value
+
+    def set_colouring(self, colour_of) -> None:
+        col = np.ascontiguousarray(colour_of, dtype=np.int32)
+        _check(self._lib.fea_plan_set_colouring(self._h, _ptr(col)))
+
+    def missing_entry(self):
+        e, r, c = c_int64(), c_int64(), c_int64()
+        _check(self._lib.fea_plan_missing_entry(self._h, byref(e), byref(r), byref(c)))
+        return None if e.value < 0 else (e.value, r.value, c.value)
+
+    @property
+    def last_launches(self) -> int:
+        return int(self._lib.fea_plan_last_launches(self._h))
+
+    # -- numeric phase ------------------------------------------------------
+    def assemble(self, K, values=None, strategy: str = "sorted", accumulate: bool = False,
+                 stream=None):
+        """values (+)= assembled K. K: cuda float64 (E, m, m); values: cuda float64 (nnz,)."""
+        import torch
+        if values is None:
+            values = torch.zeros(self.nnz, dtype=torch.float64, device=f"cuda:{self.device}")
+            accumulate = False
+        flags = N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE
+        _check(self._lib.fea_assemble(self._h, _ptr(K), STRATEGIES[strategy], _ptr(values), flags,
+                                      _stream_ptr(stream)))
+        return values
+
+    def assemble_host(self, K_host, values_host=None, strategy: str = "sorted",
+                      accumulate: bool = False, stream=None):
+        """End-to-end form: host K in, host values out (H2D + assemble + D2H, synchronous)."""
+        if values_host is None:
+            values_host = np.zeros(self.nnz, np.float64)
+            accumulate = False
+        flags = N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE
+        _check(self._lib.fea_assemble_host(self._h, _ptr(K_host), STRATEGIES[strategy],
+                                           _ptr(values_host), flags, _stream_ptr(stream)))
+        return values_host
+
+    def close(self) -> None:
+        if self._h and self._h.value:
+            self._lib.fea_plan_destroy(self._h)
+            self._h = c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def fill_seeded_k(n: int, m: int, seed: int, elem_ids=None, device: int = 0, out=None, stream=None):
+    """Seeded symmetric U[-1,1) element matrices on the device (the counter-hash supplier)."""
+    import torch
+    if out is None:
+        out = torch.empty((n, m, m), dtype=torch.float64, device=f"cuda:{device}")
+    ids = None
+    if elem_ids is not None:
+        ids = torch.as_tensor(elem_ids, dtype=torch.int64, device=out.device).contiguous()
+    _check(N.lib().fea_fill_seeded_k(_ptr(out), n, m, ctypes.c_uint64(seed), _ptr(ids),
+                                     _stream_ptr(stream)))
+    if ids is not None:
+        torch.cuda.current_stream(out.device).synchronize()
+    return out

@@ -1,0 +1,119 @@
+// Internal declarations of the B200 FE-assembly library (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/fea_gpu.h"
+
+namespace feagpu {
+
+// Exception carried to the C-ABI boundary and turned into a fea_status.
+struct Error : std::runtime_error {
+    fea_status status;
+    Error(fea_status s, const std::string& msg) : std::runtime_error(msg), status(s) {}
+};
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
+
+#define FEA_CK(x)                                                      \
+    do {                                                               \
+        cudaError_t e_ = (x);                                          \
+        if (e_ != cudaSuccess) ::feagpu::throw_cuda(e_, #x, __FILE__, __LINE__); \
+    } while (0)
+
+#define FEA_REQUIRE(cond, status, msg)                                 \
+    do {                                                               \
+        if (!(cond)) throw ::feagpu::Error((status), (msg));           \
+    } while (0)
+
+// Owning device allocation.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { reset(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+        return *this;
+    }
+    ~DevBuf() { reset(); }
+    void alloc(size_t n);
+    void reset();
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// RAII scope that makes `dev` current and restores the previous device.
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev);
+    ~DeviceScope();
+};
+
+}  // namespace feagpu
+
+// The plan: everything the numeric phase needs, resolved once (north-star
+// subsystems 1 and 2). Node-level layout — the d DOF rows of a node share one
+// column structure (pattern.cpp:85-91) — so all metadata is per node, with d
+// applied arithmetically.
+struct fea_plan {
+    int device = 0;
+    // problem shape
+    int64_t E_in = 0;        // elements given
+    int32_t m = 0;           // DOFs per element
+    int32_t d = 1;           // DOFs per node used by the plan (1 = DOF-level)
+    int32_t npe = 0;         // nodes per element = m / d
+    int64_t n_rows = 0;      // global rows
+    int64_t row_begin = 0, row_end = 0;
+    int64_t node_begin = 0, node_end = 0, n_own = 0;  // owned nodes
+    int64_t E = 0;           // kept elements
+    bool partitioned = false;
+    bool k_compact = false;
+    bool external = false;   // pattern supplied by the caller
+    // sizes
+    int64_t n_adj = 0;       // owned (node, element) incidences
+    int64_t nnz_nodes = 0;   // node-level pattern entries
+    int64_t nnz = 0;         // DOF-level values of the owned block
+    int64_t n_runs = 0;      // CRAC runs of the owned block
+    int32_t max_cnt = 0;     // longest node-level row
+    int64_t max_adj = 0;     // most elements at one node
+    int32_t pos_bytes = 1;   // 1 (uint8) or 2 (uint16) row-relative positions
+    // device metadata
+    feagpu::DevBuf conn_k;    // int32 [krows*npe] node ids, indexed by K row
+    feagpu::DevBuf elem_id;   // int64 [E] global ids of kept elements, ascending
+    feagpu::DevBuf elem_krow; // int32 [E] K row of each kept element
+    feagpu::DevBuf adj_ptr;   // int64 [n_own+1]
+    feagpu::DevBuf adj;       // int32 [n_adj] K chunk index = krow*npe + a, ascending element id per node
+    feagpu::DevBuf nptr;      // int64 [n_own+1] node-level row pointer
+    feagpu::DevBuf ncol;      // int32 [nnz_nodes] sorted neighbour node ids
+    feagpu::DevBuf nrun_ptr;  // int64 [n_own+1] exclusive scan of node-level runs
+    feagpu::DevBuf posA;      // PosT [n_adj*npe] positions, adjacency order (gather route)
+    feagpu::DevBuf posE;      // PosT [E*npe*npe] positions, element order (atomic/colour routes; lazy)
+    feagpu::DevBuf order;     // int32 [E] atomic-route element order (lazy)
+    // colouring
+    bool has_colouring = false;
+    feagpu::DevBuf colour_elems;           // int32 [E] local elements grouped by colour, ascending id
+    std::vector<int64_t> colour_off;       // n_colours+1 (host)
+    // external-pattern missing entry (lowest element)
+    int64_t miss_e = -1, miss_r = -1, miss_c = -1;
+    // bookkeeping
+    int32_t last_launches = 0;
+    feagpu::DevBuf stage_K, stage_V;       // fea_assemble_host staging
+    int64_t kbytes_required() const;
+    int64_t krows() const { return k_compact ? E : E_in; }
+};
+
+namespace feagpu {
+// numeric.cu
+void ensure_element_maps(fea_plan* p, cudaStream_t s);
+void assemble(fea_plan* p, const double* K, int strategy, double* values, uint32_t flags,
+              cudaStream_t s);
+// plan.cu helpers used by numeric.cu
+int64_t metadata_bytes(const fea_plan* p);
+}  // namespace feagpu

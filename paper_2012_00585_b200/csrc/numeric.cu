@@ -1,0 +1,522 @@
+// Numeric phase of the B200 FE-assembly library (north-star subsystem 3):
+// the scatter-add G(D(r), D(c)) += K_e(r, c) of scatter_element
+// (assembly.hpp:77-92) for all elements, with three conflict strategies.
+//
+//  FEA_DET_SORTED  k_gather   — owner-computes segmented reduction. One lane
+//      group owns a node's d rows (a contiguous block of values); it streams
+//      the node's incident element-matrix row blocks K[e][a*d .. a*d+d-1][:]
+//      (d*m contiguous doubles each) in ascending element id and folds them
+//      into a shared-memory copy of the block, then writes the block once.
+//      Per slot this is a left fold from the slot's start value in ascending
+//      element order: bit-identical to assemble_sequential (assembly.hpp:112).
+//      Every K byte is read once, every value written once, no atomics.
+//  FEA_ATOMIC      k_scatter<true>  — element owner, one fp64 atomicAdd
+//      (RED.E.ADD.F64) per entry, elements visited in a locality order
+//      (assemble_atomic, assembly.hpp:121-126).
+//  FEA_DET_COLOUR  k_scatter<false> — one launch per colour, plain
+//      load-add-store (assemble_coloured_vectorized, assembly.hpp:175-195).
+#include <cub/cub.cuh>
+
+#include <cstring>
+#include <string>
+
+#include "internal.cuh"
+
+namespace feagpu {
+extern thread_local std::string g_err;
+
+namespace {
+
+constexpr int kWarps = 4;  // warps per CTA for the numeric kernels
+
+unsigned grid_for(int64_t n, int threads) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > 148 * 64) b = 148 * 64;
+    return static_cast<unsigned>(b);
+}
+
+__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
+
+// ---------------------------------------------------------------------------
+// Deterministic owner-computes gather (sort-by-slot segmented reduction)
+// ---------------------------------------------------------------------------
+// G lanes per node; R rounds of G entries cover one d*m chunk; PF chunks are
+// in flight per group (register double-buffering for memory parallelism).
+template <int G, int R, int PF, class PosT>
+__global__ void __launch_bounds__(kWarps * 32)
+    k_gather(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
+             const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
+             const int64_t* __restrict__ nptr, int64_t n_own, int d, int npe, int acc_stride,
+             int accumulate, double* __restrict__ values) {
+    extern __shared__ double sacc[];
+    constexpr int GPW = 32 / G;
+    const int m = d * npe;
+    const int dm = d * m;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G;
+    const int gw = lane / G;
+    const int warp = threadIdx.x >> 5;
+    double* acc = sacc + static_cast<int64_t>(warp * GPW + gw) * acc_stride;
+
+    // chunk-independent decode of this lane's entries: idx -> (ki, b, kj)
+    int t_ki[R], t_b[R], t_kj[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int idx = r * G + gl;
+        const int ki = idx / m;
+        const int j = idx - ki * m;
+        const int b = j / d;
+        t_ki[r] = ki;
+        t_b[r] = idx < dm ? b : 0;
+        t_kj[r] = j - b * d;
+    }
+
+    const int64_t v = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * GPW + gw;
+    const bool active = v < n_own;
+    int64_t b0 = 0;
+    int n = 0, rowlen = 0, block = 0;
+    int64_t vb = 0;
+    if (active) {
+        b0 = adj_ptr[v];
+        n = static_cast<int>(adj_ptr[v + 1] - b0);
+        const int64_t cnt = nptr[v + 1] - nptr[v];
+        rowlen = static_cast<int>(d * cnt);
+        block = d * rowlen;
+        vb = static_cast<int64_t>(d) * d * nptr[v];
+    }
+    if (accumulate) {
+        for (int i = gl; i < block; i += G) acc[i] = values[vb + i];
+    } else {
+        for (int i = gl; i < block; i += G) acc[i] = 0.0;
+    }
+    const int n_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
+    __syncwarp();
+
+    double kv[PF][R];
+    PosT pv[PF][R];
+    auto load = [&](int p, int k) {
+        const int32_t entry = adj[b0 + k];
+        const double* src = K + static_cast<int64_t>(entry) * dm;
+        const PosT* ps = posA + (b0 + k) * npe;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int idx = r * G + gl;
+            if (idx < dm) {
+                kv[p][r] = ld_stream(src + idx);
+                pv[p][r] = ps[t_b[r]];
+            }
+        }
+    };
+#pragma unroll
+    for (int p = 0; p < PF; ++p)
+        if (p < n) load(p, p);
+
+    for (int k0 = 0; k0 < n_max; k0 += PF) {
+#pragma unroll
+        for (int p = 0; p < PF; ++p) {
+            const int k = k0 + p;
+            if (k < n) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int idx = r * G + gl;
+                    if (idx < dm) {
+                        const int s = t_ki[r] * rowlen + static_cast<int>(pv[p][r]) * d + t_kj[r];
+                        acc[s] += kv[p][r];
+                    }
+                }
+            }
+            __syncwarp();
+            if (k + PF < n) load(p, k + PF);
+        }
+    }
+    for (int i = gl; i < block; i += G) __stcs(values + vb + i, acc[i]);
+}
+
+// ---------------------------------------------------------------------------
+// Element-owner scatter: atomics (FEA_ATOMIC) or plain adds within a colour
+// ---------------------------------------------------------------------------
+// tab[idx] = a | ki<<8 | b<<16 | kj<<24 for idx = i*m + j, i = a*d+ki, j = b*d+kj.
+template <int G, class PosT, bool ATOMIC>
+__global__ void __launch_bounds__(kWarps * 32)
+    k_scatter(const double* __restrict__ K, const int32_t* __restrict__ list, int64_t n_list,
+              const int32_t* __restrict__ elem_krow, const int32_t* __restrict__ conn_k,
+              const PosT* __restrict__ posE, const int64_t* __restrict__ nptr, int64_t node_begin,
+              int64_t n_own, int d, int npe, double* __restrict__ values) {
+    extern __shared__ unsigned char smem[];
+    constexpr int GPW = 32 / G;
+    const int m = d * npe;
+    const int mm = m * m;
+    uint32_t* tab = reinterpret_cast<uint32_t*>(smem);
+    const int tab_words = (mm + 1) & ~1;
+    int64_t* rb_all = reinterpret_cast<int64_t*>(tab + tab_words);
+    int32_t* rl_all = reinterpret_cast<int32_t*>(rb_all + kWarps * GPW * npe);
+    for (int idx = threadIdx.x; idx < mm; idx += blockDim.x) {
+        const int i = idx / m, j = idx - (idx / m) * m;
+        const int a = i / d, b = j / d;
+        tab[idx] = static_cast<uint32_t>(a) | (static_cast<uint32_t>(i - a * d) << 8) |
+                   (static_cast<uint32_t>(b) << 16) | (static_cast<uint32_t>(j - b * d) << 24);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G;
+    const int gw = lane / G;
+    const int warp = threadIdx.x >> 5;
+    int64_t* rb = rb_all + (warp * GPW + gw) * npe;
+    int32_t* rl = rl_all + (warp * GPW + gw) * npe;
+    const int64_t stride_groups = ((int64_t)gridDim.x * blockDim.x >> 5) * GPW;
+    for (int64_t gi = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * GPW + gw;
+         gi - gw < n_list; gi += stride_groups) {
+        const bool active = gi < n_list;
+        int32_t le = 0, kr = 0;
+        if (active) {
+            le = list[gi];
+            kr = elem_krow[le];
+            for (int a = gl; a < npe; a += G) {
+                const int64_t v = conn_k[static_cast<int64_t>(kr) * npe + a] - node_begin;
+                const bool own = v >= 0 && v < n_own;
+                rb[a] = own ? static_cast<int64_t>(d) * d * nptr[v] : -1;
+                rl[a] = own ? static_cast<int32_t>(d * (nptr[v + 1] - nptr[v])) : 0;
+            }
+        }
+        __syncwarp();
+        if (active) {
+            const double* src = K + static_cast<int64_t>(kr) * mm;
+            const PosT* pe = posE + static_cast<int64_t>(le) * npe * npe;
+#pragma unroll 4
+            for (int idx = gl; idx < mm; idx += G) {
+                const uint32_t t = tab[idx];
+                const int a = t & 0xff, ki = (t >> 8) & 0xff, b = (t >> 16) & 0xff, kj = t >> 24;
+                const int64_t base = rb[a];
+                const double x = ld_stream(src + idx);
+                if (base >= 0) {
+                    const int64_t s = base + static_cast<int64_t>(ki) * rl[a] +
+                                      static_cast<int64_t>(pe[a * npe + b]) * d + kj;
+                    if (ATOMIC) atomicAdd(values + s, x);
+                    else values[s] += x;
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Element-order maps for the element-owner routes (built lazily)
+// ---------------------------------------------------------------------------
+template <class PosT>
+__global__ void k_pos_elem(const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
+                           int64_t n_adj, int npe, const int32_t* __restrict__ k2l,
+                           PosT* __restrict__ posE) {
+    const int64_t total = n_adj * npe;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = t / npe;
+        const int b = static_cast<int>(t - k * npe);
+        const int32_t entry = adj[k];
+        const int32_t kr = entry / npe;
+        const int a = entry - kr * npe;
+        const int64_t le = k2l ? k2l[kr] : kr;
+        posE[(le * npe + a) * npe + b] = posA[t];
+    }
+}
+
+__global__ void k_k2l(const int32_t* __restrict__ elem_krow, int64_t E, int32_t* __restrict__ k2l) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
+         i += (int64_t)gridDim.x * blockDim.x)
+        k2l[elem_krow[i]] = static_cast<int32_t>(i);
+}
+
+// consecutive-element node sharing (locality test) and min-node sort keys
+__global__ void k_locality(const int32_t* __restrict__ conn_k, const int32_t* __restrict__ elem_krow,
+                           int64_t E, int npe, unsigned long long* shared_pairs,
+                           uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t* c = conn_k + static_cast<int64_t>(elem_krow[i]) * npe;
+        uint32_t mn = 0xffffffffu;
+        for (int a = 0; a < npe; ++a) mn = min(mn, static_cast<uint32_t>(c[a]));
+        keys[i] = mn;
+        vals[i] = static_cast<int32_t>(i);
+        if (i > 0) {
+            const int32_t* q = conn_k + static_cast<int64_t>(elem_krow[i - 1]) * npe;
+            bool sh = false;
+            for (int a = 0; a < npe && !sh; ++a)
+                for (int b = 0; b < npe; ++b)
+                    if (c[a] == q[b]) { sh = true; break; }
+            if (sh) atomicAdd(shared_pairs, 1ull);
+        }
+    }
+}
+
+__global__ void k_iota32(int32_t* x, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = static_cast<int32_t>(i);
+}
+
+__device__ __forceinline__ double kval(uint64_t seed, int64_t e, int i, int j) {
+    auto mix = [](uint64_t x) {
+        uint64_t z = x + 0x9e3779b97f4a7c15ULL;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        return z ^ (z >> 31);
+    };
+    const uint64_t lo = static_cast<uint64_t>(i < j ? i : j);
+    const uint64_t hi = static_cast<uint64_t>(i < j ? j : i);
+    const uint64_t h = mix(mix(seed + static_cast<uint64_t>(e)) ^ ((lo << 32) | hi));
+    return static_cast<double>(h >> 11) * 0x1p-53 * 2.0 - 1.0;
+}
+
+__global__ void k_fill_k(double* __restrict__ K, int64_t n, int m, uint64_t seed,
+                         const int64_t* __restrict__ ids) {
+    const int64_t mm = static_cast<int64_t>(m) * m;
+    const int64_t total = n * mm;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = t / mm;
+        const int rem = static_cast<int>(t - e * mm);
+        const int i = rem / m, j = rem - (rem / m) * m;
+        K[t] = kval(seed, ids ? ids[e] : e, i, j);
+    }
+}
+
+template <class F>
+void cub_call(F&& f) {
+    size_t tb = 0;
+    FEA_CK(f(nullptr, tb));
+    DevBuf t;
+    t.alloc(tb);
+    FEA_CK(f(t.p, tb));
+}
+
+// --- launch helpers --------------------------------------------------------
+
+template <int G, int R, int PF, class PosT>
+void run_gather(fea_plan* p, const double* K, double* values, bool accumulate, cudaStream_t s) {
+    constexpr int GPW = 32 / G;
+    const int acc_stride = p->d * p->d * p->max_cnt + 1;  // +1 staggers groups across banks
+    size_t smem = static_cast<size_t>(kWarps) * GPW * acc_stride * sizeof(double);
+    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID,
+                "node row block too large for shared-memory accumulation");
+    auto kern = k_gather<G, R, PF, PosT>;
+    if (smem > 48 * 1024)
+        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t groups = p->n_own;
+    const int64_t blocks = (groups + kWarps * GPW - 1) / (kWarps * GPW);
+    if (blocks == 0) return;
+    kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
+        K, p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->posA.as<PosT>(),
+        p->nptr.as<int64_t>(), p->n_own, p->d, p->npe, acc_stride, accumulate ? 1 : 0, values);
+    FEA_CK(cudaGetLastError());
+    p->last_launches += 1;
+}
+
+template <class PosT>
+void gather(fea_plan* p, const double* K, double* values, bool accumulate, cudaStream_t s) {
+    const int dm = p->d * p->m;
+    if (dm <= 4) run_gather<4, 1, 8, PosT>(p, K, values, accumulate, s);
+    else if (dm <= 8) run_gather<8, 1, 8, PosT>(p, K, values, accumulate, s);
+    else if (dm <= 16) run_gather<16, 1, 4, PosT>(p, K, values, accumulate, s);
+    else if (dm <= 32) run_gather<32, 1, 4, PosT>(p, K, values, accumulate, s);
+    else if (dm == 72) run_gather<8, 9, 2, PosT>(p, K, values, accumulate, s);
+    else if (dm <= 128) run_gather<32, 4, 2, PosT>(p, K, values, accumulate, s);
+    else if (dm <= 256) run_gather<32, 8, 2, PosT>(p, K, values, accumulate, s);
+    else if (dm <= 512) run_gather<32, 16, 1, PosT>(p, K, values, accumulate, s);
+    else throw Error(FEA_ERR_INVALID, "element row block (d*m) larger than 512 entries");
+}
+
+template <int G, class PosT, bool ATOMIC>
+void run_scatter(fea_plan* p, const double* K, const int32_t* list, int64_t n_list, double* values,
+                 cudaStream_t s) {
+    if (n_list == 0) return;
+    constexpr int GPW = 32 / G;
+    const int mm = p->m * p->m;
+    const size_t smem = static_cast<size_t>((mm + 1) & ~1) * 4 +
+                        static_cast<size_t>(kWarps) * GPW * p->npe * (8 + 4);
+    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "element matrix too large for the scatter kernel");
+    auto kern = k_scatter<G, PosT, ATOMIC>;
+    if (smem > 48 * 1024)
+        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t blocks = std::min<int64_t>((n_list + kWarps * GPW - 1) / (kWarps * GPW), 148 * 16);
+    kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
+        K, list, n_list, p->elem_krow.as<int32_t>(), p->conn_k.as<int32_t>(), p->posE.as<PosT>(),
+        p->nptr.as<int64_t>(), p->node_begin, p->n_own, p->d, p->npe, values);
+    FEA_CK(cudaGetLastError());
+    p->last_launches += 1;
+}
+
+template <class PosT, bool ATOMIC>
+void scatter(fea_plan* p, const double* K, const int32_t* list, int64_t n_list, double* values,
+             cudaStream_t s) {
+    const int mm = p->m * p->m;
+    if (mm <= 4) run_scatter<4, PosT, ATOMIC>(p, K, list, n_list, values, s);
+    else if (mm <= 8) run_scatter<8, PosT, ATOMIC>(p, K, list, n_list, values, s);
+    else if (mm <= 16) run_scatter<16, PosT, ATOMIC>(p, K, list, n_list, values, s);
+    else run_scatter<32, PosT, ATOMIC>(p, K, list, n_list, values, s);
+}
+
+}  // namespace
+
+void ensure_element_maps(fea_plan* p, cudaStream_t s) {
+    if (p->posE.p && p->order.p) return;
+    const int64_t n = p->E * p->npe * p->npe;
+    p->posE.alloc(n * p->pos_bytes);
+    FEA_CK(cudaMemsetAsync(p->posE.p, 0xff, p->posE.bytes, s));
+    DevBuf k2l;
+    const int32_t* k2l_ptr = nullptr;
+    if (p->partitioned && !p->k_compact) {
+        k2l.alloc(p->E_in * 4);
+        if (p->E > 0)
+            k_k2l<<<grid_for(p->E, 256), 256, 0, s>>>(p->elem_krow.as<int32_t>(), p->E,
+                                                      k2l.as<int32_t>());
+        k2l_ptr = k2l.as<int32_t>();
+    }
+    if (p->n_adj > 0) {
+        if (p->pos_bytes == 1)
+            k_pos_elem<uint8_t><<<grid_for(p->n_adj * p->npe, 256), 256, 0, s>>>(
+                p->adj.as<int32_t>(), p->posA.as<uint8_t>(), p->n_adj, p->npe, k2l_ptr,
+                p->posE.as<uint8_t>());
+        else
+            k_pos_elem<uint16_t><<<grid_for(p->n_adj * p->npe, 256), 256, 0, s>>>(
+                p->adj.as<int32_t>(), p->posA.as<uint16_t>(), p->n_adj, p->npe, k2l_ptr,
+                p->posE.as<uint16_t>());
+    }
+    FEA_CK(cudaGetLastError());
+    // Atomic-route element order: keep the caller's order when consecutive
+    // elements already share nodes (>= half the pairs), else visit elements
+    // sorted by their lowest node id so concurrently resident CTAs hit the
+    // same rows and the reductions stay in L2.
+    p->order.alloc(p->E * 4);
+    if (p->E > 0) {
+        DevBuf keys, vals, keys2, cnt;
+        keys.alloc(p->E * 4);
+        vals.alloc(p->E * 4);
+        keys2.alloc(p->E * 4);
+        cnt.alloc(8);
+        FEA_CK(cudaMemsetAsync(cnt.p, 0, 8, s));
+        k_locality<<<grid_for(p->E, 256), 256, 0, s>>>(p->conn_k.as<int32_t>(),
+                                                       p->elem_krow.as<int32_t>(), p->E, p->npe,
+                                                       cnt.as<unsigned long long>(),
+                                                       keys.as<uint32_t>(), vals.as<int32_t>());
+        FEA_CK(cudaGetLastError());
+        unsigned long long shared = 0;
+        FEA_CK(cudaMemcpyAsync(&shared, cnt.p, 8, cudaMemcpyDeviceToHost, s));
+        FEA_CK(cudaStreamSynchronize(s));
+        if (2 * static_cast<int64_t>(shared) >= p->E - 1) {
+            k_iota32<<<grid_for(p->E, 256), 256, 0, s>>>(p->order.as<int32_t>(), p->E);
+        } else {
+            cub_call([&](void* t, size_t& tb) {
+                return cub::DeviceRadixSort::SortPairs(t, tb, keys.as<uint32_t>(),
+                                                       keys2.as<uint32_t>(), vals.as<int32_t>(),
+                                                       p->order.as<int32_t>(), (int)p->E, 0, 32, s);
+            });
+        }
+        FEA_CK(cudaGetLastError());
+        FEA_CK(cudaStreamSynchronize(s));
+    }
+}
+
+void assemble(fea_plan* p, const double* K, int strategy, double* values, uint32_t flags,
+              cudaStream_t s) {
+    FEA_REQUIRE(strategy == FEA_ATOMIC || strategy == FEA_DET_SORTED || strategy == FEA_DET_COLOUR,
+                FEA_ERR_INVALID, "unknown strategy");
+    if (p->miss_e >= 0) {
+        char buf[160];
+        std::snprintf(buf, sizeof(buf),
+                      "assembly hit a coefficient missing from the pattern: element %lld, (%lld, %lld)",
+                      static_cast<long long>(p->miss_e), static_cast<long long>(p->miss_r),
+                      static_cast<long long>(p->miss_c));
+        throw Error(FEA_ERR_MISSING_ENTRY, buf);
+    }
+    FEA_REQUIRE(p->nnz == 0 || values, FEA_ERR_INVALID, "values is NULL");
+    FEA_REQUIRE(p->E == 0 || K, FEA_ERR_INVALID, "K is NULL");
+    const bool overwrite = (flags & FEA_OVERWRITE) != 0;
+    p->last_launches = 0;
+    if (strategy == FEA_DET_SORTED) {
+        if (p->pos_bytes == 1) gather<uint8_t>(p, K, values, !overwrite, s);
+        else gather<uint16_t>(p, K, values, !overwrite, s);
+        return;
+    }
+    if (strategy == FEA_DET_COLOUR)
+        FEA_REQUIRE(p->has_colouring, FEA_ERR_INVALID,
+                    "FEA_DET_COLOUR needs a colouring (fea_plan_set_colouring)");
+    ensure_element_maps(p, s);
+    if (overwrite && p->nnz > 0) FEA_CK(cudaMemsetAsync(values, 0, p->nnz * 8, s));
+    if (strategy == FEA_ATOMIC) {
+        if (p->pos_bytes == 1) scatter<uint8_t, true>(p, K, p->order.as<int32_t>(), p->E, values, s);
+        else scatter<uint16_t, true>(p, K, p->order.as<int32_t>(), p->E, values, s);
+        return;
+    }
+    const int nc = static_cast<int>(p->colour_off.size()) - 1;
+    for (int c = 0; c < nc; ++c) {
+        const int32_t* list = p->colour_elems.as<int32_t>() + p->colour_off[c];
+        const int64_t cnt = p->colour_off[c + 1] - p->colour_off[c];
+        if (p->pos_bytes == 1) scatter<uint8_t, false>(p, K, list, cnt, values, s);
+        else scatter<uint16_t, false>(p, K, list, cnt, values, s);
+    }
+}
+
+}  // namespace feagpu
+
+using namespace feagpu;
+
+namespace {
+template <class F>
+fea_status guarded_n(F&& f) {
+    try {
+        g_err.clear();
+        f();
+        return FEA_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.status;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FEA_ERR_INVALID;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+fea_status fea_assemble(fea_plan* plan, const double* K, int32_t strategy, double* values,
+                        uint32_t flags, void* stream) {
+    return guarded_n([&] {
+        FEA_REQUIRE(plan, FEA_ERR_INVALID, "plan is NULL");
+        DeviceScope ds(plan->device);
+        assemble(plan, K, strategy, values, flags, static_cast<cudaStream_t>(stream));
+    });
+}
+
+fea_status fea_assemble_host(fea_plan* plan, const double* K_host, int32_t strategy,
+                             double* values_host, uint32_t flags, void* stream) {
+    return guarded_n([&] {
+        FEA_REQUIRE(plan, FEA_ERR_INVALID, "plan is NULL");
+        DeviceScope ds(plan->device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const size_t kb = static_cast<size_t>(plan->kbytes_required());
+        const size_t vb = static_cast<size_t>(plan->nnz) * 8;
+        if (plan->stage_K.bytes < kb) plan->stage_K.alloc(kb);
+        if (plan->stage_V.bytes < vb) plan->stage_V.alloc(vb);
+        if (kb) FEA_CK(cudaMemcpyAsync(plan->stage_K.p, K_host, kb, cudaMemcpyHostToDevice, s));
+        if (!(flags & FEA_OVERWRITE) && vb)
+            FEA_CK(cudaMemcpyAsync(plan->stage_V.p, values_host, vb, cudaMemcpyHostToDevice, s));
+        assemble(plan, plan->stage_K.as<double>(), strategy, plan->stage_V.as<double>(), flags, s);
+        if (vb) FEA_CK(cudaMemcpyAsync(values_host, plan->stage_V.p, vb, cudaMemcpyDeviceToHost, s));
+        FEA_CK(cudaStreamSynchronize(s));
+    });
+}
+
+fea_status fea_fill_seeded_k(double* K, int64_t n, int32_t m, uint64_t seed,
+                             const int64_t* elem_ids, void* stream) {
+    return guarded_n([&] {
+        FEA_REQUIRE(n >= 0 && m >= 1 && (n == 0 || K), FEA_ERR_INVALID, "bad arguments");
+        if (n == 0) return;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        k_fill_k<<<grid_for(n * m * m, 256), 256, 0, s>>>(K, n, m, seed, elem_ids);
+        FEA_CK(cudaGetLastError());
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,1176 @@
+// Symbolic phase of the B200 FE-assembly library (north-star subsystem 1) and
+// the per-element local->global slot map (subsystem 2), plus the plan's C ABI.
+//
+// Reference behaviour restated (not translated):
+//   build_pattern         pattern.cpp:24-108  node->element index, per-node
+//                         gather + sort/unique, replicate to the node's d rows
+//   count_pattern_runs    pattern.cpp:110-120
+//   build_crac_arrays     formats.cpp:21-41
+//   CsrBase/CracBase::locate formats.hpp:165-199, :276-290 (external patterns)
+//   greedy_colouring      colouring.cpp:24-75
+//   find_colour_conflict  colouring.cpp:91-119
+//
+// B200 layout: everything is stored per NODE (the d rows of a node share one
+// column list, pattern.cpp:85-91) and expanded arithmetically:
+//   row (v,k) of the owned block starts at  d*d*nptr[v] + k*d*cnt(v)
+//   entry (v,k ; u,kj) lives at             row_start + d*pos(v,u) + kj
+// so the slot map is one small row-relative position per (element, node a,
+// node b) — uint8 when every node row has <= 256 neighbour nodes — instead of
+// an int32/int64 slot per element-matrix entry.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "internal.cuh"
+
+namespace feagpu {
+
+thread_local std::string g_err;
+
+void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+    cudaGetLastError();  // clear sticky-free errors
+    const fea_status s = (e == cudaErrorMemoryAllocation) ? FEA_ERR_OOM : FEA_ERR_CUDA;
+    throw Error(s, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                       std::to_string(line) + ")");
+}
+
+void DevBuf::alloc(size_t n) {
+    reset();
+    bytes = n;
+    FEA_CK(cudaMalloc(&p, n < 256 ? 256 : n));
+}
+
+void DevBuf::reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+}
+
+DeviceScope::DeviceScope(int dev) {
+    FEA_CK(cudaGetDevice(&prev));
+    if (prev != dev) FEA_CK(cudaSetDevice(dev));
+}
+DeviceScope::~DeviceScope() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+}
+
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr int kNodeCap = 512;  // candidates sorted in a warp's shared-memory slice
+
+bool is_device_ptr(const void* ptr) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+template <class F>
+void cub_call(F&& f) {
+    size_t tb = 0;
+    FEA_CK(f(nullptr, tb));
+    DevBuf t;
+    t.alloc(tb);
+    FEA_CK(f(t.p, tb));
+}
+
+unsigned grid_for(int64_t n, int threads) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > 148 * 64) b = 148 * 64;  // grid-stride beyond ~64 CTAs per SM
+    return static_cast<unsigned>(b);
+}
+
+int bits_for(uint64_t x) {
+    int b = 1;
+    while (b < 64 && (x >> b) != 0) ++b;
+    return b;
+}
+
+// ---------------------------------------------------------------------------
+// Kernels
+// ---------------------------------------------------------------------------
+
+// Flat DOFs -> node ids, validating range and (for d > 1) the node-contiguous
+// layout dof(v,k) = v*d+k (dof_map.hpp:59). flags bit0: layout broken,
+// bit1: DOF out of [0, n_rows) (the reference's out_of_range, dof_map.cpp:82-84).
+__global__ void k_extract_conn(const int64_t* __restrict__ dofs, int64_t total, int m, int d,
+                               int npe, int64_t n_rows, int32_t* __restrict__ conn,
+                               unsigned* flags) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = t / npe;
+        const int a = static_cast<int>(t - e * npe);
+        const int64_t* src = dofs + e * m + (int64_t)a * d;
+        const int64_t base = src[0];
+        unsigned f = 0;
+        if (base < 0 || base >= n_rows) f |= 2u;
+        if (d > 1) {
+            if (base % d != 0) f |= 1u;
+            for (int k = 1; k < d; ++k) {
+                const int64_t x = src[k];
+                if (x != base + k) f |= 1u;
+                if (x < 0 || x >= n_rows) f |= 2u;
+            }
+        }
+        if (f) atomicOr(flags, f);
+        conn[t] = static_cast<int32_t>(base / d);
+    }
+}
+
+__global__ void k_keep_flags(const int32_t* __restrict__ conn, int64_t E, int npe, int64_t nb,
+                             int64_t ne, int64_t* __restrict__ keep) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t k = 0;
+        for (int a = 0; a < npe; ++a) {
+            const int64_t v = conn[e * npe + a];
+            k |= (v >= nb && v < ne) ? 1 : 0;
+        }
+        keep[e] = k;
+    }
+}
+
+__global__ void k_scatter_kept(const int64_t* __restrict__ keep, const int64_t* __restrict__ pos,
+                               int64_t E, int64_t* __restrict__ elem_id) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x)
+        if (keep[e]) elem_id[pos[e]] = e;
+}
+
+__global__ void k_iota64(int64_t* x, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = i;
+}
+
+__global__ void k_krow(const int64_t* __restrict__ elem_id, int64_t E, bool compact,
+                       int32_t* __restrict__ krow) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
+         i += (int64_t)gridDim.x * blockDim.x)
+        krow[i] = static_cast<int32_t>(compact ? i : elem_id[i]);
+}
+
+__global__ void k_gather_conn(const int32_t* __restrict__ conn_all, const int64_t* __restrict__ elem_id,
+                              int64_t E, int npe, int32_t* __restrict__ conn) {
+    const int64_t total = E * npe;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t le = t / npe;
+        conn[t] = conn_all[elem_id[le] * npe + (t - le * npe)];
+    }
+}
+
+// (node, element) incidences, emitted in ascending element order; the stable
+// radix sort by node then leaves each node's list in ascending element id —
+// the node->element index of pattern.cpp:32-48.
+__global__ void k_emit_incidences(const int32_t* __restrict__ conn_k,
+                                  const int32_t* __restrict__ krow, int64_t E, int npe,
+                                  int64_t nb, int64_t ne, uint32_t* __restrict__ keys,
+                                  int32_t* __restrict__ vals,
+                                  unsigned long long* __restrict__ counts) {
+    const int64_t total = E * npe;
+    const uint32_t sentinel = static_cast<uint32_t>(ne - nb);
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t le = t / npe;
+        const int a = static_cast<int>(t - le * npe);
+        const int64_t kr = krow[le];
+        const int64_t v = conn_k[kr * npe + a];
+        const bool own = v >= nb && v < ne;
+        keys[t] = own ? static_cast<uint32_t>(v - nb) : sentinel;
+        vals[t] = static_cast<int32_t>(kr * npe + a);
+        if (own) atomicAdd(counts + (v - nb), 1ull);
+    }
+}
+
+__device__ __forceinline__ int32_t candidate(const int32_t* __restrict__ adj,
+                                             const int32_t* __restrict__ conn_k, int64_t b0,
+                                             int npe, int64_t i) {
+    const int64_t k = i / npe;
+    const int b = static_cast<int>(i - k * npe);
+    const int32_t entry = adj[b0 + k];
+    return conn_k[(int64_t)(entry - entry % npe) + b];
+}
+
+// Warp-level bitonic sort of s[0..P), P a power of two.
+__device__ void warp_bitonic(int32_t* s, int P, int lane) {
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < P; i += 32) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const int32_t a = s[i], b = s[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        s[i] = b;
+                        s[ixj] = a;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// Per owned node: gather the node ids of every adjacent element, sort, unique
+// (pattern.cpp:66-83, on node ids instead of DOFs — the d-expansion is exact).
+// FILL=false: counts[v] = #unique; FILL=true: writes the list at ncol+nptr[v].
+// Nodes with more than kNodeCap candidates are deferred to k_node_pattern_big.
+template <bool FILL>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_node_pattern(const int64_t* __restrict__ adj_ptr, const int32_t* __restrict__ adj,
+                   const int32_t* __restrict__ conn_k, int npe, int64_t n_own,
+                   int64_t* __restrict__ counts, const int64_t* __restrict__ nptr,
+                   int32_t* __restrict__ ncol, int32_t* __restrict__ big_list,
+                   unsigned* __restrict__ n_big, unsigned* __restrict__ max_big) {
+    __shared__ int32_t sh[kWarpsPerBlock][kNodeCap];
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    int32_t* s = sh[w];
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n_own;
+         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t b0 = adj_ptr[v];
+        const int64_t nc = (adj_ptr[v + 1] - b0) * npe;
+        if (nc > kNodeCap) {
+            if (!FILL && lane == 0) {
+                big_list[atomicAdd(n_big, 1u)] = static_cast<int32_t>(v);
+                atomicMax(max_big, static_cast<unsigned>(nc));
+            }
+            continue;
+        }
+        int P = 1;
+        while (P < nc) P <<= 1;
+        for (int i = lane; i < P; i += 32)
+            s[i] = i < nc ? candidate(adj, conn_k, b0, npe, i) : INT32_MAX;
+        __syncwarp();
+        warp_bitonic(s, P, lane);
+        int64_t out = FILL ? nptr[v] : 0;
+        int total = 0;
+        for (int i0 = 0; i0 < P; i0 += 32) {
+            const int i = i0 + lane;
+            const bool uniq = i < P && s[i] != INT32_MAX && (i == 0 || s[i] != s[i - 1]);
+            const unsigned bal = __ballot_sync(0xffffffffu, uniq);
+            if (FILL && uniq) ncol[out + total + __popc(bal & ((1u << lane) - 1u))] = s[i];
+            total += __popc(bal);
+        }
+        if (!FILL && lane == 0) counts[v] = total;
+        __syncwarp();
+    }
+}
+
+// Block-per-node fallback for high-valence nodes (dynamic shared memory).
+template <bool FILL>
+__global__ void k_node_pattern_big(const int64_t* __restrict__ adj_ptr,
+                                   const int32_t* __restrict__ adj,
+                                   const int32_t* __restrict__ conn_k, int npe,
+                                   const int32_t* __restrict__ big_list, int64_t* __restrict__ counts,
+                                   const int64_t* __restrict__ nptr, int32_t* __restrict__ ncol) {
+    extern __shared__ int32_t s[];
+    const int64_t v = big_list[blockIdx.x];
+    const int64_t b0 = adj_ptr[v];
+    const int64_t nc = (adj_ptr[v + 1] - b0) * npe;
+    int P = 1;
+    while (P < nc) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x)
+        s[i] = i < nc ? candidate(adj, conn_k, b0, npe, i) : INT32_MAX;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const int32_t a = s[i], b = s[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        s[i] = b;
+                        s[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    if (threadIdx.x == 0) {
+        int64_t total = 0;
+        const int64_t out = FILL ? nptr[v] : 0;
+        for (int i = 0; i < P && s[i] != INT32_MAX; ++i)
+            if (i == 0 || s[i] != s[i - 1]) {
+                if (FILL) ncol[out + total] = s[i];
+                ++total;
+            }
+        if (!FILL) counts[v] = total;
+    }
+}
+
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t* __restrict__ a, int64_t n,
+                                                   int32_t x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Slot map in adjacency order: for incidence k = (element, a) of node v and
+// every node b of the element, the position of node b in v's sorted list.
+// This is the per-entry locate() of scatter_element (assembly.hpp:84),
+// resolved once for all entries sharing a (row node, column node) block.
+template <class PosT>
+__global__ void k_pos_adj(const int64_t* __restrict__ adj_ptr, const int32_t* __restrict__ adj,
+                          const int32_t* __restrict__ conn_k, int npe, int64_t n_own,
+                          const int64_t* __restrict__ nptr, const int32_t* __restrict__ ncol,
+                          PosT* __restrict__ posA) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n_own;
+         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t b0 = adj_ptr[v];
+        const int64_t nc = (adj_ptr[v + 1] - b0) * npe;
+        const int32_t* list = ncol + nptr[v];
+        const int64_t cnt = nptr[v + 1] - nptr[v];
+        for (int64_t i = lane; i < nc; i += 32) {
+            const int32_t u = candidate(adj, conn_k, b0, npe, i);
+            posA[b0 * npe + i] = static_cast<PosT>(lower_bound_i32(list, cnt, u));
+        }
+    }
+}
+
+// Node-level CRAC run count (pattern.cpp:110-120 / formats.cpp:29 restated per
+// node: column blocks of consecutive nodes merge into one run).
+__global__ void k_node_runs(const int64_t* __restrict__ nptr, const int32_t* __restrict__ ncol,
+                            int64_t n_own, int64_t* __restrict__ runs) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n_own;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = 0;
+        for (int64_t i = nptr[v]; i < nptr[v + 1]; ++i)
+            if (i == nptr[v] || ncol[i] != ncol[i - 1] + 1) ++r;
+        runs[v] = r;
+    }
+}
+
+__global__ void k_max_i64(const int64_t* __restrict__ x, int64_t n, unsigned long long* out) {
+    unsigned long long m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, static_cast<unsigned long long>(x[i]));
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+__global__ void k_diff(const int64_t* __restrict__ ptr, int64_t n, int64_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = ptr[i + 1] - ptr[i];
+}
+
+// CSR expansion of the node-level pattern (the SparsityPattern of
+// pattern.hpp:29-35 for the owned block).
+__global__ void k_expand_csr(const int64_t* __restrict__ nptr, const int32_t* __restrict__ ncol,
+                             int64_t n_own, int d, int64_t node_begin, int64_t* __restrict__ row_ptr,
+                             int64_t* __restrict__ cols) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n_own;
+         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t cnt = nptr[v + 1] - nptr[v];
+        const int64_t base = (int64_t)d * d * nptr[v];
+        const int64_t rowlen = d * cnt;
+        if (lane < d) row_ptr[v * d + lane] = base + lane * rowlen;
+        if (v == n_own - 1 && lane == 0) row_ptr[n_own * d] = (int64_t)d * d * nptr[n_own];
+        const int32_t* list = ncol + nptr[v];
+        for (int64_t i = lane; i < d * rowlen; i += 32) {
+            const int64_t k = i / rowlen;
+            const int64_t q = i - k * rowlen;
+            const int64_t p = q / d;
+            cols[base + i] = (int64_t)list[p] * d + (q - p * d);
+        }
+    }
+    (void)node_begin;
+}
+
+// CRAC arrays of the owned block (build_crac_arrays, formats.cpp:21-41):
+// row_ptr in col_align entry units; (column start, values position) per run;
+// the final (0, nnz) pair.
+__global__ void k_expand_crac(const int64_t* __restrict__ nptr, const int32_t* __restrict__ ncol,
+                              const int64_t* __restrict__ nrun_ptr, int64_t n_own, int d,
+                              int64_t* __restrict__ crac_ptr, int64_t* __restrict__ col_align) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n_own;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t cnt = nptr[v + 1] - nptr[v];
+        const int64_t nr = nrun_ptr[v + 1] - nrun_ptr[v];
+        const int32_t* list = ncol + nptr[v];
+        for (int k = 0; k < d; ++k) {
+            const int64_t r = v * d + k;
+            int64_t w = 2 * ((int64_t)d * nrun_ptr[v] + k * nr);
+            crac_ptr[r] = w;
+            const int64_t row_start = (int64_t)d * d * nptr[v] + (int64_t)k * d * cnt;
+            for (int64_t p = 0; p < cnt; ++p)
+                if (p == 0 || list[p] != list[p - 1] + 1) {
+                    col_align[w++] = (int64_t)list[p] * d;
+                    col_align[w++] = row_start + p * d;
+                }
+        }
+        if (v == n_own - 1) {
+            const int64_t tot = 2 * (int64_t)d * nrun_ptr[n_own];
+            crac_ptr[n_own * d] = tot;
+            col_align[tot] = 0;
+            col_align[tot + 1] = (int64_t)d * d * nptr[n_own];
+        }
+    }
+}
+
+// External patterns: locate every element entry in the caller's CSR pattern
+// (lower-bound search; the reference switches linear/binary at 30 entries,
+// formats.hpp:196-199 — the found position is identical) or CRAC pattern
+// (Listing 1 linear block search, formats.hpp:276-290). Each warp takes one
+// incidence row at a time, its lanes the element's columns. Missing entries
+// record the lowest (element, local row, local col) — the first one
+// scatter_element would hit (assembly.hpp:80-88).
+template <class PosT, bool CRAC>
+__global__ void k_pos_external(const int64_t* __restrict__ adj_ptr, const int32_t* __restrict__ adj,
+                               const int32_t* __restrict__ conn_k, int npe, int64_t n_rows,
+                               const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ cols,
+                               const int64_t* __restrict__ crac_ptr,
+                               const int64_t* __restrict__ col_align, PosT* __restrict__ posA,
+                               unsigned long long* __restrict__ miss) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n_rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t b0 = adj_ptr[r];
+        const int64_t nc = (adj_ptr[r + 1] - b0) * npe;
+        const int64_t lo0 = row_ptr[r], hi0 = row_ptr[r + 1];
+        for (int64_t i = lane; i < nc; i += 32) {
+            const int64_t c = candidate(adj, conn_k, b0, npe, i);
+            int64_t pos = -1;
+            if (!CRAC) {
+                int64_t lo = lo0, hi = hi0;
+                while (lo < hi) {
+                    const int64_t mid = lo + (hi - lo) / 2;
+                    if (cols[mid] < c) lo = mid + 1;
+                    else hi = mid;
+                }
+                if (lo < hi0 && cols[lo] == c) pos = lo;
+            } else {
+                int64_t j = crac_ptr[r];
+                const int64_t row_end = crac_ptr[r + 1];
+                if (j != row_end) {
+                    while (j + 2 < row_end && col_align[j + 2] <= c) j += 2;
+                    const int64_t cs = col_align[j], vs = col_align[j + 1], ve = col_align[j + 3];
+                    if (c >= cs && c < cs + (ve - vs)) pos = vs + (c - cs);
+                }
+            }
+            if (pos < 0) {
+                const int32_t entry = adj[b0 + i / npe];
+                const int64_t e = entry / npe;  // external plans: K row == element id
+                const int a = entry % npe;
+                const int b = static_cast<int>(i % npe);
+                atomicMin(miss, static_cast<unsigned long long>((e * npe + a) * npe + b));
+                pos = lo0;
+            }
+            posA[b0 * npe + i] = static_cast<PosT>(pos - lo0);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Host orchestration
+// ---------------------------------------------------------------------------
+
+struct Tmp {
+    DevBuf buf;
+    template <class T>
+    T* alloc(size_t n) {
+        buf.alloc(n * sizeof(T));
+        return buf.as<T>();
+    }
+};
+
+// Upload (or alias) the element DOF array.
+const int64_t* device_dofs(const int64_t* elem_dofs, int64_t n, DevBuf& hold, cudaStream_t s) {
+    if (n == 0) return nullptr;
+    if (is_device_ptr(elem_dofs)) return elem_dofs;
+    hold.alloc(n * sizeof(int64_t));
+    FEA_CK(cudaMemcpyAsync(hold.p, elem_dofs, n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    return hold.as<int64_t>();
+}
+
+// Node->element incidences + adjacency (shared by own and external patterns).
+void build_adjacency(fea_plan* p, cudaStream_t s) {
+    const int64_t items = p->E * p->npe;
+    FEA_REQUIRE(items < (int64_t{1} << 31) && p->krows() * p->npe < (int64_t{1} << 31),
+                FEA_ERR_INVALID, "more than 2^31 element-node incidences are not supported");
+    DevBuf counts_b;
+    counts_b.alloc((p->n_own + 1) * sizeof(int64_t));
+    FEA_CK(cudaMemsetAsync(counts_b.p, 0, counts_b.bytes, s));
+    DevBuf keys_in, vals_in, keys_out, vals_out;
+    keys_in.alloc(items * 4);
+    vals_in.alloc(items * 4);
+    keys_out.alloc(items * 4);
+    vals_out.alloc(items * 4);
+    if (items > 0) {
+        k_emit_incidences<<<grid_for(items, 256), 256, 0, s>>>(
+            p->conn_k.as<int32_t>(), p->elem_krow.as<int32_t>(), p->E, p->npe, p->node_begin,
+            p->node_end, keys_in.as<uint32_t>(), vals_in.as<int32_t>(),
+            counts_b.as<unsigned long long>());
+        FEA_CK(cudaGetLastError());
+        const int end_bit = bits_for(static_cast<uint64_t>(p->n_own));
+        cub_call([&](void* t, size_t& tb) {
+            return cub::DeviceRadixSort::SortPairs(t, tb, keys_in.as<uint32_t>(),
+                                                   keys_out.as<uint32_t>(), vals_in.as<int32_t>(),
+                                                   vals_out.as<int32_t>(), (int)items, 0, end_bit, s);
+        });
+    }
+    p->adj_ptr.alloc((p->n_own + 1) * sizeof(int64_t));
+    cub_call([&](void* t, size_t& tb) {
+        return cub::DeviceScan::ExclusiveSum(t, tb, counts_b.as<int64_t>(), p->adj_ptr.as<int64_t>(),
+                                             (int)(p->n_own + 1), s);
+    });
+    FEA_CK(cudaMemcpyAsync(&p->n_adj, p->adj_ptr.as<int64_t>() + p->n_own, sizeof(int64_t),
+                           cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaStreamSynchronize(s));
+    p->adj.alloc(p->n_adj * 4);
+    if (p->n_adj > 0)
+        FEA_CK(cudaMemcpyAsync(p->adj.p, vals_out.p, p->n_adj * 4, cudaMemcpyDeviceToDevice, s));
+    // largest node incidence count (reporting / sizing)
+    {
+        DevBuf cnt, mx;
+        cnt.alloc(p->n_own * 8 + 8);
+        mx.alloc(8);
+        FEA_CK(cudaMemsetAsync(mx.p, 0, 8, s));
+        if (p->n_own > 0) {
+            k_diff<<<grid_for(p->n_own, 256), 256, 0, s>>>(p->adj_ptr.as<int64_t>(), p->n_own,
+                                                           cnt.as<int64_t>());
+            k_max_i64<<<grid_for(p->n_own, 256), 256, 0, s>>>(cnt.as<int64_t>(), p->n_own,
+                                                              mx.as<unsigned long long>());
+            FEA_CK(cudaGetLastError());
+        }
+        unsigned long long h = 0;
+        FEA_CK(cudaMemcpyAsync(&h, mx.p, 8, cudaMemcpyDeviceToHost, s));
+        FEA_CK(cudaStreamSynchronize(s));
+        p->max_adj = static_cast<int64_t>(h);
+    }
+}
+
+void finish_counts(fea_plan* p, DevBuf& counts, cudaStream_t s) {
+    p->nptr.alloc((p->n_own + 1) * sizeof(int64_t));
+    cub_call([&](void* t, size_t& tb) {
+        return cub::DeviceScan::ExclusiveSum(t, tb, counts.as<int64_t>(), p->nptr.as<int64_t>(),
+                                             (int)(p->n_own + 1), s);
+    });
+    DevBuf mx;
+    mx.alloc(8);
+    FEA_CK(cudaMemsetAsync(mx.p, 0, 8, s));
+    if (p->n_own > 0)
+        k_max_i64<<<grid_for(p->n_own, 256), 256, 0, s>>>(counts.as<int64_t>(), p->n_own,
+                                                          mx.as<unsigned long long>());
+    FEA_CK(cudaGetLastError());
+    unsigned long long h = 0;
+    FEA_CK(cudaMemcpyAsync(&h, mx.p, 8, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaMemcpyAsync(&p->nnz_nodes, p->nptr.as<int64_t>() + p->n_own, 8,
+                           cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaStreamSynchronize(s));
+    FEA_REQUIRE(h <= 65536, FEA_ERR_INVALID,
+                "a pattern row has more than 65536 column nodes (position map limit)");
+    p->max_cnt = static_cast<int32_t>(h);
+    p->pos_bytes = h <= 256 ? 1 : 2;
+    p->nnz = static_cast<int64_t>(p->d) * p->d * p->nnz_nodes;
+}
+
+void build_runs(fea_plan* p, cudaStream_t s) {
+    DevBuf runs;
+    runs.alloc((p->n_own + 1) * sizeof(int64_t));
+    FEA_CK(cudaMemsetAsync(runs.p, 0, runs.bytes, s));
+    if (p->n_own > 0)
+        k_node_runs<<<grid_for(p->n_own, 256), 256, 0, s>>>(p->nptr.as<int64_t>(),
+                                                            p->ncol.as<int32_t>(), p->n_own,
+                                                            runs.as<int64_t>());
+    FEA_CK(cudaGetLastError());
+    p->nrun_ptr.alloc((p->n_own + 1) * sizeof(int64_t));
+    cub_call([&](void* t, size_t& tb) {
+        return cub::DeviceScan::ExclusiveSum(t, tb, runs.as<int64_t>(), p->nrun_ptr.as<int64_t>(),
+                                             (int)(p->n_own + 1), s);
+    });
+    int64_t nr = 0;
+    FEA_CK(cudaMemcpyAsync(&nr, p->nrun_ptr.as<int64_t>() + p->n_own, 8, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaStreamSynchronize(s));
+    p->n_runs = nr * p->d;
+}
+
+void build_own_pattern(fea_plan* p, cudaStream_t s) {
+    const unsigned blocks = grid_for(p->n_own * 32, kWarpsPerBlock * 32);
+    DevBuf counts, big, nbig, maxbig;
+    counts.alloc((p->n_own + 1) * sizeof(int64_t));
+    FEA_CK(cudaMemsetAsync(counts.p, 0, counts.bytes, s));
+    big.alloc((p->n_own + 1) * 4);
+    nbig.alloc(4);
+    maxbig.alloc(4);
+    FEA_CK(cudaMemsetAsync(nbig.p, 0, 4, s));
+    FEA_CK(cudaMemsetAsync(maxbig.p, 0, 4, s));
+    if (p->n_own > 0)
+        k_node_pattern<false><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
+            p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
+            p->n_own, counts.as<int64_t>(), nullptr, nullptr, big.as<int32_t>(),
+            nbig.as<unsigned>(), maxbig.as<unsigned>());
+    FEA_CK(cudaGetLastError());
+    unsigned h_nbig = 0, h_maxbig = 0;
+    FEA_CK(cudaMemcpyAsync(&h_nbig, nbig.p, 4, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaMemcpyAsync(&h_maxbig, maxbig.p, 4, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaStreamSynchronize(s));
+    size_t big_smem = 0;
+    if (h_nbig > 0) {
+        unsigned P = 1;
+        while (P < h_maxbig) P <<= 1;
+        big_smem = static_cast<size_t>(P) * 4;
+        FEA_REQUIRE(big_smem <= 200 * 1024, FEA_ERR_INVALID,
+                    "node valence too high for the symbolic phase (> 51200 candidate nodes)");
+        FEA_CK(cudaFuncSetAttribute(k_node_pattern_big<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_smem));
+        FEA_CK(cudaFuncSetAttribute(k_node_pattern_big<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_smem));
+        k_node_pattern_big<false><<<h_nbig, 256, big_smem, s>>>(
+            p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
+            big.as<int32_t>(), counts.as<int64_t>(), nullptr, nullptr);
+        FEA_CK(cudaGetLastError());
+    }
+    finish_counts(p, counts, s);
+    p->ncol.alloc(p->nnz_nodes * 4);
+    if (p->n_own > 0)
+        k_node_pattern<true><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
+            p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
+            p->n_own, nullptr, p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), big.as<int32_t>(),
+            nbig.as<unsigned>(), maxbig.as<unsigned>());
+    if (h_nbig > 0)
+        k_node_pattern_big<true><<<h_nbig, 256, big_smem, s>>>(
+            p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
+            big.as<int32_t>(), nullptr, p->nptr.as<int64_t>(), p->ncol.as<int32_t>());
+    FEA_CK(cudaGetLastError());
+    // slot map (adjacency order)
+    p->posA.alloc(p->n_adj * p->npe * p->pos_bytes);
+    if (p->n_own > 0) {
+        if (p->pos_bytes == 1)
+            k_pos_adj<uint8_t><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
+                p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
+                p->n_own, p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->posA.as<uint8_t>());
+        else
+            k_pos_adj<uint16_t><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
+                p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
+                p->n_own, p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->posA.as<uint16_t>());
+        FEA_CK(cudaGetLastError());
+    }
+    build_runs(p, s);
+}
+
+// Common front end: DOFs -> node connectivity (with node-layout detection),
+// kept elements, K-row mapping.
+void build_elements(fea_plan* p, const int64_t* elem_dofs, int32_t d_hint, cudaStream_t s) {
+    DevBuf hold;
+    const int64_t* ddofs = device_dofs(elem_dofs, p->E_in * p->m, hold, s);
+    DevBuf flags;
+    flags.alloc(4);
+    DevBuf conn_all;
+    int d = (d_hint > 1 && p->m % d_hint == 0) ? d_hint : 1;
+    for (;;) {
+        const int npe = p->m / d;
+        FEA_CK(cudaMemsetAsync(flags.p, 0, 4, s));
+        conn_all.alloc(p->E_in * npe * 4);
+        if (p->E_in > 0) {
+            k_extract_conn<<<grid_for(p->E_in * npe, 256), 256, 0, s>>>(
+                ddofs, p->E_in * npe, p->m, d, npe, p->n_rows, conn_all.as<int32_t>(),
+                flags.as<unsigned>());
+            FEA_CK(cudaGetLastError());
+        }
+        unsigned h = 0;
+        FEA_CK(cudaMemcpyAsync(&h, flags.p, 4, cudaMemcpyDeviceToHost, s));
+        FEA_CK(cudaStreamSynchronize(s));
+        FEA_REQUIRE(!(h & 2u), FEA_ERR_INVALID, "element DOF outside [0, n_rows)");
+        if ((h & 1u) && d > 1) {
+            d = 1;  // not node-contiguous: DOF-level plan
+            continue;
+        }
+        p->d = d;
+        p->npe = npe;
+        break;
+    }
+    FEA_REQUIRE(p->row_begin % p->d == 0 && p->row_end % p->d == 0, FEA_ERR_INVALID,
+                "row range must align to node boundaries (multiples of dofs_per_node)");
+    const int64_t n_nodes = p->n_rows / p->d;
+    FEA_REQUIRE(n_nodes < (int64_t{1} << 31) - 1, FEA_ERR_INVALID, "more than 2^31 nodes");
+    p->node_begin = p->row_begin / p->d;
+    p->node_end = p->row_end / p->d;
+    p->n_own = p->node_end - p->node_begin;
+    p->partitioned = !(p->row_begin == 0 && p->row_end == p->n_rows);
+    if (!p->partitioned) {
+        p->E = p->E_in;
+        p->elem_id.alloc(p->E * 8);
+        if (p->E > 0) k_iota64<<<grid_for(p->E, 256), 256, 0, s>>>(p->elem_id.as<int64_t>(), p->E);
+        p->conn_k = std::move(conn_all);
+    } else {
+        DevBuf keep, pos;
+        keep.alloc((p->E_in + 1) * 8);
+        pos.alloc((p->E_in + 1) * 8);
+        FEA_CK(cudaMemsetAsync(keep.p, 0, keep.bytes, s));
+        if (p->E_in > 0)
+            k_keep_flags<<<grid_for(p->E_in, 256), 256, 0, s>>>(
+                conn_all.as<int32_t>(), p->E_in, p->npe, p->node_begin, p->node_end,
+                keep.as<int64_t>());
+        cub_call([&](void* t, size_t& tb) {
+            return cub::DeviceScan::ExclusiveSum(t, tb, keep.as<int64_t>(), pos.as<int64_t>(),
+                                                 (int)(p->E_in + 1), s);
+        });
+        FEA_CK(cudaMemcpyAsync(&p->E, pos.as<int64_t>() + p->E_in, 8, cudaMemcpyDeviceToHost, s));
+        FEA_CK(cudaStreamSynchronize(s));
+        p->elem_id.alloc(p->E * 8);
+        if (p->E_in > 0)
+            k_scatter_kept<<<grid_for(p->E_in, 256), 256, 0, s>>>(keep.as<int64_t>(),
+                                                                  pos.as<int64_t>(), p->E_in,
+                                                                  p->elem_id.as<int64_t>());
+        if (p->k_compact) {
+            p->conn_k.alloc(p->E * p->npe * 4);
+            if (p->E > 0)
+                k_gather_conn<<<grid_for(p->E * p->npe, 256), 256, 0, s>>>(
+                    conn_all.as<int32_t>(), p->elem_id.as<int64_t>(), p->E, p->npe,
+                    p->conn_k.as<int32_t>());
+        } else {
+            p->conn_k = std::move(conn_all);
+        }
+    }
+    FEA_CK(cudaGetLastError());
+    p->elem_krow.alloc(p->E * 4);
+    if (p->E > 0)
+        k_krow<<<grid_for(p->E, 256), 256, 0, s>>>(p->elem_id.as<int64_t>(), p->E,
+                                                   p->k_compact || !p->partitioned,
+                                                   p->elem_krow.as<int32_t>());
+    FEA_CK(cudaGetLastError());
+}
+
+struct Stream {
+    cudaStream_t s = nullptr;
+    Stream() { FEA_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+    ~Stream() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
+template <class F>
+fea_status guarded(F&& f) {
+    try {
+        g_err.clear();
+        f();
+        return FEA_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return FEA_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FEA_ERR_INVALID;
+    }
+}
+
+// Copy n bytes from a device buffer to a host-or-device destination.
+void copy_out(void* dst, const void* src, size_t n, cudaStream_t s) {
+    if (n == 0) return;
+    FEA_CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDefault, s));
+}
+
+// Host-side conn of the kept elements, in ascending element id.
+std::vector<int32_t> host_conn(const fea_plan* p, cudaStream_t s) {
+    std::vector<int32_t> h(static_cast<size_t>(p->E * p->npe));
+    std::vector<int32_t> kr(static_cast<size_t>(p->E));
+    if (p->E == 0) return h;
+    std::vector<int32_t> all(static_cast<size_t>(p->krows() * p->npe));
+    FEA_CK(cudaMemcpyAsync(all.data(), p->conn_k.p, all.size() * 4, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaMemcpyAsync(kr.data(), p->elem_krow.p, kr.size() * 4, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaStreamSynchronize(s));
+    for (int64_t e = 0; e < p->E; ++e)
+        std::memcpy(&h[e * p->npe], &all[static_cast<size_t>(kr[e]) * p->npe], p->npe * 4);
+    return h;
+}
+
+}  // namespace
+
+int64_t metadata_bytes(const fea_plan* p) {
+    return static_cast<int64_t>(p->conn_k.bytes + p->elem_id.bytes + p->elem_krow.bytes +
+                                p->adj_ptr.bytes + p->adj.bytes + p->nptr.bytes + p->ncol.bytes +
+                                p->nrun_ptr.bytes + p->posA.bytes + p->posE.bytes +
+                                p->order.bytes + p->colour_elems.bytes);
+}
+
+}  // namespace feagpu
+
+int64_t fea_plan::kbytes_required() const { return krows() * static_cast<int64_t>(m) * m * 8; }
+
+using namespace feagpu;
+
+extern "C" {
+
+const char* fea_last_error(void) { return g_err.c_str(); }
+
+int fea_version(void) { return 100; }
+
+fea_status fea_plan_create(int device, const int64_t* elem_dofs, int64_t n_elements, int32_t m,
+                           int64_t n_rows, int32_t dofs_per_node, int64_t row_begin,
+                           int64_t row_end, uint32_t flags, fea_plan** out) {
+    return guarded([&] {
+        FEA_REQUIRE(out, FEA_ERR_INVALID, "out is NULL");
+        *out = nullptr;
+        FEA_REQUIRE(n_elements >= 0 && m >= 1 && n_rows >= 0, FEA_ERR_INVALID,
+                    "need n_elements >= 0, m >= 1, n_rows >= 0");
+        FEA_REQUIRE(n_elements == 0 || elem_dofs, FEA_ERR_INVALID, "elem_dofs is NULL");
+        FEA_REQUIRE(dofs_per_node >= 1, FEA_ERR_INVALID, "dofs_per_node must be >= 1");
+        FEA_REQUIRE(0 <= row_begin && row_begin <= row_end && row_end <= n_rows, FEA_ERR_INVALID,
+                    "row range must satisfy 0 <= row_begin <= row_end <= n_rows");
+        DeviceScope ds(device);
+        Stream st;
+        auto p = std::make_unique<fea_plan>();
+        p->device = device;
+        p->E_in = n_elements;
+        p->m = m;
+        p->n_rows = n_rows;
+        p->row_begin = row_begin;
+        p->row_end = row_end;
+        p->k_compact = (flags & FEA_PLAN_K_COMPACT) != 0;
+        build_elements(p.get(), elem_dofs, dofs_per_node, st.s);
+        build_adjacency(p.get(), st.s);
+        build_own_pattern(p.get(), st.s);
+        FEA_CK(cudaStreamSynchronize(st.s));
+        *out = p.release();
+    });
+}
+
+fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, int64_t n_elements,
+                                        int32_t m, int64_t n_rows, int32_t format,
+                                        const int64_t* row_ptr, const int64_t* idx,
+                                        fea_plan** out) {
+    return guarded([&] {
+        FEA_REQUIRE(out, FEA_ERR_INVALID, "out is NULL");
+        *out = nullptr;
+        FEA_REQUIRE(format == FEA_FORMAT_CSR || format == FEA_FORMAT_CRAC, FEA_ERR_INVALID,
+                    "unknown pattern format");
+        FEA_REQUIRE(n_elements >= 0 && m >= 1 && n_rows >= 0 && row_ptr && (n_rows == 0 || idx),
+                    FEA_ERR_INVALID, "bad arguments");
+        FEA_REQUIRE(n_rows < (int64_t{1} << 31) - 1, FEA_ERR_INVALID, "more than 2^31 rows");
+        DeviceScope ds(device);
+        Stream st;
+        cudaStream_t s = st.s;
+        // Host copies of the caller's pattern (reference arrays live on the host).
+        const bool dev_in = is_device_ptr(row_ptr);
+        std::vector<int64_t> h_ptr(static_cast<size_t>(n_rows + 1));
+        FEA_CK(cudaMemcpy(h_ptr.data(), row_ptr, h_ptr.size() * 8, cudaMemcpyDefault));
+        std::vector<int64_t> h_csr_ptr, h_cols, h_crac_ptr, h_align;
+        if (format == FEA_FORMAT_CSR) {
+            h_csr_ptr = h_ptr;
+            h_cols.resize(static_cast<size_t>(h_ptr[n_rows]));
+            if (!h_cols.empty())
+                FEA_CK(cudaMemcpy(h_cols.data(), idx, h_cols.size() * 8, cudaMemcpyDefault));
+        } else {
+            h_crac_ptr = h_ptr;
+            const int64_t n_align = h_ptr[n_rows] + 2;
+            h_align.resize(static_cast<size_t>(n_align));
+            FEA_CK(cudaMemcpy(h_align.data(), idx, h_align.size() * 8, cudaMemcpyDefault));
+            // CSR view of the CRAC pattern (for_each_in_row, formats.hpp:315-324)
+            h_csr_ptr.resize(static_cast<size_t>(n_rows + 1));
+            for (int64_t r = 0; r < n_rows; ++r) {
+                h_csr_ptr[r] = h_align[h_crac_ptr[r] + 1];
+                for (int64_t i = h_crac_ptr[r]; i < h_crac_ptr[r + 1]; i += 2) {
+                    const int64_t cs = h_align[i], vs = h_align[i + 1], ve = h_align[i + 3];
+                    for (int64_t k = 0; k < ve - vs; ++k) h_cols.push_back(cs + k);
+                }
+            }
+            h_csr_ptr[n_rows] = static_cast<int64_t>(h_cols.size());
+            if (n_rows > 0) h_csr_ptr[0] = 0;
+        }
+        (void)dev_in;
+        for (int64_t r = 0; r < n_rows; ++r) {
+            FEA_REQUIRE(h_csr_ptr[r] <= h_csr_ptr[r + 1], FEA_ERR_INVALID, "row_ptr not monotone");
+            for (int64_t i = h_csr_ptr[r]; i < h_csr_ptr[r + 1]; ++i) {
+                FEA_REQUIRE(h_cols[i] >= 0 && h_cols[i] < n_rows, FEA_ERR_INVALID,
+                            "pattern column outside the matrix");
+                FEA_REQUIRE(i == h_csr_ptr[r] || h_cols[i - 1] < h_cols[i], FEA_ERR_INVALID,
+                            "pattern columns not strictly ascending within a row");
+            }
+        }
+        auto p = std::make_unique<fea_plan>();
+        p->device = device;
+        p->external = true;
+        p->E_in = n_elements;
+        p->m = m;
+        p->n_rows = n_rows;
+        p->row_begin = 0;
+        p->row_end = n_rows;
+        build_elements(p.get(), elem_dofs, 1, s);
+        build_adjacency(p.get(), s);
+        // node-level pattern == the caller's pattern (d = 1)
+        const int64_t nnz = h_csr_ptr[n_rows];
+        p->nptr.alloc((n_rows + 1) * 8);
+        FEA_CK(cudaMemcpyAsync(p->nptr.p, h_csr_ptr.data(), (n_rows + 1) * 8,
+                               cudaMemcpyHostToDevice, s));
+        std::vector<int32_t> h_cols32(h_cols.begin(), h_cols.end());
+        p->ncol.alloc(nnz * 4);
+        if (nnz > 0)
+            FEA_CK(cudaMemcpyAsync(p->ncol.p, h_cols32.data(), nnz * 4, cudaMemcpyHostToDevice, s));
+        int64_t max_len = 0;
+        for (int64_t r = 0; r < n_rows; ++r) max_len = std::max(max_len, h_csr_ptr[r + 1] - h_csr_ptr[r]);
+        FEA_REQUIRE(max_len <= 65536, FEA_ERR_INVALID, "pattern row longer than 65536 entries");
+        p->max_cnt = static_cast<int32_t>(max_len);
+        p->pos_bytes = max_len <= 256 ? 1 : 2;
+        p->nnz_nodes = nnz;
+        p->nnz = nnz;
+        // device copies for the lookup kernel
+        DevBuf d_ptr, d_cols, d_cptr, d_align, miss;
+        d_ptr.alloc((n_rows + 1) * 8);
+        FEA_CK(cudaMemcpyAsync(d_ptr.p, h_csr_ptr.data(), (n_rows + 1) * 8, cudaMemcpyHostToDevice, s));
+        d_cols.alloc(nnz * 8);
+        if (nnz > 0)
+            FEA_CK(cudaMemcpyAsync(d_cols.p, h_cols.data(), nnz * 8, cudaMemcpyHostToDevice, s));
+        if (format == FEA_FORMAT_CRAC) {
+            d_cptr.alloc((n_rows + 1) * 8);
+            d_align.alloc(h_align.size() * 8);
+            FEA_CK(cudaMemcpyAsync(d_cptr.p, h_crac_ptr.data(), (n_rows + 1) * 8,
+                                   cudaMemcpyHostToDevice, s));
+            FEA_CK(cudaMemcpyAsync(d_align.p, h_align.data(), h_align.size() * 8,
+                                   cudaMemcpyHostToDevice, s));
+        }
+        miss.alloc(8);
+        FEA_CK(cudaMemsetAsync(miss.p, 0xff, 8, s));
+        p->posA.alloc(p->n_adj * p->npe * p->pos_bytes);
+        const unsigned blocks = grid_for(n_rows * 32, 256);
+        if (n_rows > 0) {
+#define FEA_LAUNCH_EXT(T, C)                                                                   \
+    k_pos_external<T, C><<<blocks, 256, 0, s>>>(                                               \
+        p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe, n_rows, \
+        d_ptr.as<int64_t>(), d_cols.as<int64_t>(), d_cptr.as<int64_t>(), d_align.as<int64_t>(), \
+        p->posA.as<T>(), miss.as<unsigned long long>())
+            const bool crac = format == FEA_FORMAT_CRAC;
+            if (p->pos_bytes == 1) {
+                if (crac) FEA_LAUNCH_EXT(uint8_t, true); else FEA_LAUNCH_EXT(uint8_t, false);
+            } else {
+                if (crac) FEA_LAUNCH_EXT(uint16_t, true); else FEA_LAUNCH_EXT(uint16_t, false);
+            }
+#undef FEA_LAUNCH_EXT
+            FEA_CK(cudaGetLastError());
+        }
+        unsigned long long hm = 0;
+        FEA_CK(cudaMemcpyAsync(&hm, miss.p, 8, cudaMemcpyDeviceToHost, s));
+        FEA_CK(cudaStreamSynchronize(s));
+        if (hm != ~0ull) {
+            const int64_t mm = static_cast<int64_t>(p->m) * p->m;
+            const int64_t e = static_cast<int64_t>(hm) / mm;
+            const int64_t rem = static_cast<int64_t>(hm) - e * mm;
+            const int a = static_cast<int>(rem / p->m), b = static_cast<int>(rem % p->m);
+            std::vector<int64_t> hd(static_cast<size_t>(p->m));
+            FEA_CK(cudaMemcpy(hd.data(), elem_dofs + e * p->m, p->m * 8, cudaMemcpyDefault));
+            p->miss_e = e;
+            p->miss_r = hd[a];
+            p->miss_c = hd[b];
+        }
+        build_runs(p.get(), s);
+        FEA_CK(cudaStreamSynchronize(s));
+        *out = p.release();
+    });
+}
+
+void fea_plan_destroy(fea_plan* plan) {
+    if (!plan) return;
+    try {
+        DeviceScope ds(plan->device);
+        delete plan;
+    } catch (...) {
+        delete plan;
+    }
+}
+
+fea_status fea_plan_sizes(const fea_plan* p, int64_t* n_rows, int64_t* nnz, int64_t* n_runs,
+                          int64_t* n_elements) {
+    return guarded([&] {
+        FEA_REQUIRE(p, FEA_ERR_INVALID, "plan is NULL");
+        if (n_rows) *n_rows = p->n_own * p->d;
+        if (nnz) *nnz = p->nnz;
+        if (n_runs) *n_runs = p->n_runs;
+        if (n_elements) *n_elements = p->E;
+    });
+}
+
+fea_status fea_plan_info(const fea_plan* p, int32_t* dofs_per_node, int32_t* nodes_per_element,
+                         int64_t* meta) {
+    return guarded([&] {
+        FEA_REQUIRE(p, FEA_ERR_INVALID, "plan is NULL");
+        if (dofs_per_node) *dofs_per_node = p->d;
+        if (nodes_per_element) *nodes_per_element = p->npe;
+        if (meta) *meta = metadata_bytes(p);
+    });
+}
+
+fea_status fea_plan_copy_csr(const fea_plan* p, int64_t* row_ptr, int64_t* cols) {
+    return guarded([&] {
+        FEA_REQUIRE(p && row_ptr && (p->nnz == 0 || cols), FEA_ERR_INVALID, "NULL argument");
+        DeviceScope ds(p->device);
+        Stream st;
+        const int64_t rows = p->n_own * p->d;
+        DevBuf drp, dcols;
+        drp.alloc((rows + 1) * 8);
+        dcols.alloc(p->nnz * 8);
+        FEA_CK(cudaMemsetAsync(drp.p, 0, 8, st.s));
+        if (p->n_own > 0)
+            k_expand_csr<<<grid_for(p->n_own * 32, 256), 256, 0, st.s>>>(
+                p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->n_own, p->d, p->node_begin,
+                drp.as<int64_t>(), dcols.as<int64_t>());
+        FEA_CK(cudaGetLastError());
+        copy_out(row_ptr, drp.p, (rows + 1) * 8, st.s);
+        copy_out(cols, dcols.p, p->nnz * 8, st.s);
+        FEA_CK(cudaStreamSynchronize(st.s));
+    });
+}
+
+fea_status fea_plan_copy_crac(const fea_plan* p, int64_t* row_ptr, int64_t* col_align) {
+    return guarded([&] {
+        FEA_REQUIRE(p && row_ptr && col_align, FEA_ERR_INVALID, "NULL argument");
+        DeviceScope ds(p->device);
+        Stream st;
+        const int64_t rows = p->n_own * p->d;
+        DevBuf dptr, dal;
+        dptr.alloc((rows + 1) * 8);
+        dal.alloc((2 * p->n_runs + 2) * 8);
+        if (p->n_own > 0) {
+            k_expand_crac<<<grid_for(p->n_own, 128), 128, 0, st.s>>>(
+                p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->nrun_ptr.as<int64_t>(), p->n_own,
+                p->d, dptr.as<int64_t>(), dal.as<int64_t>());
+            FEA_CK(cudaGetLastError());
+        } else {
+            const int64_t z[2] = {0, 0};
+            FEA_CK(cudaMemcpyAsync(dptr.p, z, 8, cudaMemcpyHostToDevice, st.s));
+            FEA_CK(cudaMemcpyAsync(dal.p, z, 16, cudaMemcpyHostToDevice, st.s));
+        }
+        copy_out(row_ptr, dptr.p, (rows + 1) * 8, st.s);
+        copy_out(col_align, dal.p, (2 * p->n_runs + 2) * 8, st.s);
+        FEA_CK(cudaStreamSynchronize(st.s));
+    });
+}
+
+fea_status fea_plan_copy_elements(const fea_plan* p, int64_t* elem_ids) {
+    return guarded([&] {
+        FEA_REQUIRE(p && (p->E == 0 || elem_ids), FEA_ERR_INVALID, "NULL argument");
+        DeviceScope ds(p->device);
+        FEA_CK(cudaMemcpy(elem_ids, p->elem_id.p, p->E * 8, cudaMemcpyDefault));
+    });
+}
+
+// greedy_colouring (colouring.cpp:24-75) over the plan's elements in ascending
+// id. Inherently sequential (each element depends on all earlier ones): host.
+fea_status fea_plan_greedy_colouring(const fea_plan* p, int32_t* colour_of, int32_t* n_colours) {
+    return guarded([&] {
+        FEA_REQUIRE(p && (p->E == 0 || colour_of), FEA_ERR_INVALID, "NULL argument");
+        DeviceScope ds(p->device);
+        Stream st;
+        const std::vector<int32_t> conn = host_conn(p, st.s);
+        const int npe = p->npe;
+        int64_t n_nodes = 0;
+        for (const int32_t v : conn) n_nodes = std::max<int64_t>(n_nodes, v + 1);
+        std::vector<int64_t> ptr(static_cast<size_t>(n_nodes) + 1, 0);
+        for (const int32_t v : conn) ++ptr[v + 1];
+        for (int64_t v = 0; v < n_nodes; ++v) ptr[v + 1] += ptr[v];
+        std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+        std::vector<int32_t> adj(conn.size());
+        for (int64_t e = 0; e < p->E; ++e)
+            for (int a = 0; a < npe; ++a) adj[fill[conn[e * npe + a]]++] = static_cast<int32_t>(e);
+        std::vector<int32_t> col(static_cast<size_t>(p->E), -1);
+        std::vector<char> used;
+        int nc = 0;
+        for (int64_t e = 0; e < p->E; ++e) {
+            std::fill(used.begin(), used.end(), 0);
+            for (int a = 0; a < npe; ++a) {
+                const int32_t v = conn[e * npe + a];
+                for (int64_t k = ptr[v]; k < ptr[v + 1]; ++k) {
+                    const int c = col[adj[k]];
+                    if (c >= 0) {
+                        if (static_cast<size_t>(c) >= used.size()) used.resize(c + 1, 0);
+                        used[c] = 1;
+                    }
+                }
+            }
+            int c = 0;
+            while (static_cast<size_t>(c) < used.size() && used[c]) ++c;
+            col[e] = c;
+            nc = std::max(nc, c + 1);
+        }
+        std::memcpy(colour_of, col.data(), col.size() * 4);
+        if (n_colours) *n_colours = nc;
+    });
+}
+
+fea_status fea_plan_set_colouring(fea_plan* p, const int32_t* colour_of) {
+    return guarded([&] {
+        FEA_REQUIRE(p && (p->E == 0 || colour_of), FEA_ERR_INVALID, "NULL argument");
+        DeviceScope ds(p->device);
+        Stream st;
+        std::vector<int32_t> col(static_cast<size_t>(p->E));
+        if (p->E > 0) FEA_CK(cudaMemcpy(col.data(), colour_of, col.size() * 4, cudaMemcpyDefault));
+        int nc = 0;
+        for (const int32_t c : col) {
+            FEA_REQUIRE(c >= 0, FEA_ERR_INVALID, "negative colour");
+            nc = std::max(nc, c + 1);
+        }
+        // find_colour_conflict (colouring.cpp:91-119): same-colour elements may
+        // not share a DOF; with node-contiguous DOFs that is sharing a node.
+        const std::vector<int32_t> conn = host_conn(p, st.s);
+        const int npe = p->npe;
+        std::vector<int64_t> off(static_cast<size_t>(nc) + 1, 0);
+        for (const int32_t c : col) ++off[c + 1];
+        for (int c = 0; c < nc; ++c) off[c + 1] += off[c];
+        std::vector<int32_t> by_colour(col.size());
+        {
+            std::vector<int64_t> f(off.begin(), off.end() - 1);
+            for (int64_t e = 0; e < p->E; ++e) by_colour[f[col[e]]++] = static_cast<int32_t>(e);
+        }
+        int64_t n_nodes = 0;
+        for (const int32_t v : conn) n_nodes = std::max<int64_t>(n_nodes, v + 1);
+        std::vector<int64_t> owner(static_cast<size_t>(n_nodes), -1);
+        for (int c = 0; c < nc; ++c) {
+            for (int64_t i = off[c]; i < off[c + 1]; ++i) {
+                const int32_t e = by_colour[i];
+                for (int a = 0; a < npe; ++a) {
+                    const int32_t v = conn[static_cast<int64_t>(e) * npe + a];
+                    if (owner[v] >= 0 && owner[v] != e)
+                        throw Error(FEA_ERR_INVALID_COLOURING,
+                                    "invalid colouring: elements " + std::to_string(owner[v]) +
+                                        " and " + std::to_string(e) + " share dof " +
+                                        std::to_string(static_cast<int64_t>(v) * p->d) +
+                                        " within one colour");
+                    owner[v] = e;
+                }
+            }
+            for (int64_t i = off[c]; i < off[c + 1]; ++i)
+                for (int a = 0; a < npe; ++a)
+                    owner[conn[static_cast<int64_t>(by_colour[i]) * npe + a]] = -1;
+        }
+        p->colour_elems.alloc(by_colour.size() * 4);
+        if (!by_colour.empty())
+            FEA_CK(cudaMemcpy(p->colour_elems.p, by_colour.data(), by_colour.size() * 4,
+                              cudaMemcpyHostToDevice));
+        p->colour_off = off;
+        p->has_colouring = true;
+    });
+}
+
+fea_status fea_plan_missing_entry(const fea_plan* p, int64_t* element, int64_t* row, int64_t* col) {
+    return guarded([&] {
+        FEA_REQUIRE(p, FEA_ERR_INVALID, "plan is NULL");
+        if (element) *element = p->miss_e;
+        if (row) *row = p->miss_r;
+        if (col) *col = p->miss_c;
+    });
+}
+
+int32_t fea_plan_last_launches(const fea_plan* p) { return p ? p->last_launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,242 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Patterns and CRAC arrays: bit-exact int64 arrays (build_pattern pattern.cpp:24-108,
+build_crac_arrays formats.cpp:21-41). Values: FEA_DET_SORTED bit-exact vs
+assemble_sequential (assembly.hpp:112-118); FEA_DET_COLOUR bit-exact vs
+assemble_coloured_vectorized (assembly.hpp:175-195) under the same greedy colouring;
+FEA_ATOMIC within |a-b| <= 1e-12*max(|a|,|b|,1) (test_assembly.cpp:236).
+"""
+import numpy as np
+import pytest
+
+from paper_2012_00585_b200 import meshgen as M
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12  # reference tolerance form, test_assembly.cpp:236 / acceptance.cpp:281
+
+CASES = [
+    ("quad4", 6, 1, None),
+    ("quad4", 5, 4, "nodes"),
+    ("hex8", 3, 3, "elements"),
+    ("hex8", 4, 2, None),
+    ("tet4", 4, 1, "nodes"),
+    ("tet4", 3, 3, None),
+    ("hex27", 2, 3, None),
+    ("hex27", 3, 1, "elements"),
+]
+
+
+def close(a, b, tol=TOL):
+    return np.all(np.abs(a - b) <= tol * np.maximum(np.maximum(np.abs(a), np.abs(b)), 1.0))
+
+
+def problem(mesh, n, d, perm):
+    conn, nn = M.make_mesh(mesh, n, perm)
+    return conn, nn, M.element_dofs(conn, d), nn * d
+
+
+@pytest.mark.parametrize("mesh,n,d,perm", CASES)
+def test_pattern_bit_exact(gpu, orc, mesh, n, d, perm):
+    conn, nn, ed, n_rows = problem(mesh, n, d, perm)
+    P = orc.Pattern.build(conn, nn, d)
+    with gpu.Plan(ed, n_rows, dofs_per_node=d) as plan:
+        assert plan.dofs_per_node == d
+        assert (plan.n_rows, plan.nnz, plan.n_runs) == (P.n_rows, P.nnz, P.n_runs)
+        rp, cs = plan.csr()
+        orp, ocs = P.arrays()
+        assert np.array_equal(rp, orp) and np.array_equal(cs, ocs)
+        cp, ca = plan.crac()
+        ocp, oca = P.crac()
+        assert np.array_equal(cp, ocp) and np.array_equal(ca, oca)
+    if perm is None:
+        assert P.nnz == M.closed_form_nnz(mesh, n, d)
+
+
+@pytest.mark.parametrize("mesh,n,d,perm", CASES)
+def test_seeded_k_matches_oracle(gpu, orc, mesh, n, d, perm):
+    conn, nn, ed, n_rows = problem(mesh, n, d, perm)
+    K = gpu.fill_seeded_k(conn.shape[0], ed.shape[1], 42).cpu().numpy()
+    assert K.tobytes() == orc.fill_k(42, conn.shape[0], ed.shape[1]).tobytes()
+    assert np.array_equal(K, np.swapaxes(K, 1, 2))
+
+
+@pytest.mark.parametrize("mesh,n,d,perm", CASES)
+def test_values_all_strategies(gpu, orc, mesh, n, d, perm):
+    import torch
+    conn, nn, ed, n_rows = problem(mesh, n, d, perm)
+    P = orc.Pattern.build(conn, nn, d)
+    Kh = orc.fill_k(42, conn.shape[0], ed.shape[1])
+    want_seq = P.assemble_sequential(ed, Kh)
+    col, nc = orc.greedy_colouring(conn, nn)
+    want_col = P.assemble_coloured(ed, Kh, col)
+    K = torch.from_numpy(Kh).cuda()
+    with gpu.Plan(ed, n_rows, dofs_per_node=d) as plan:
+        got = plan.assemble(K, strategy="sorted").cpu().numpy()
+        assert got.tobytes() == want_seq.tobytes()
+        gcol, gnc = plan.greedy_colouring()
+        assert np.array_equal(gcol, col) and gnc == nc
+        plan.set_colouring(gcol)
+        got_c = plan.assemble(K, strategy="colour").cpu().numpy()
+        assert got_c.tobytes() == want_col.tobytes()
+        got_a = plan.assemble(K, strategy="atomic").cpu().numpy()
+        assert close(got_a, want_seq)
+
+
+@pytest.mark.parametrize("mesh,n,d,perm", CASES[:5])
+def test_ones_bitwise_and_conservation(gpu, orc, mesh, n, d, perm):
+    """acceptance.cpp:180-199 / verify.cpp:85-100: with ones K every route is bitwise equal
+    to sequential and the total is exactly E*m^2."""
+    import torch
+    conn, nn, ed, n_rows = problem(mesh, n, d, perm)
+    E, m = ed.shape
+    P = orc.Pattern.build(conn, nn, d)
+    want = P.assemble_sequential(ed, np.ones((E, m, m)))
+    K = torch.ones((E, m, m), dtype=torch.float64, device="cuda")
+    with gpu.Plan(ed, n_rows, dofs_per_node=d) as plan:
+        col, _ = plan.greedy_colouring()
+        plan.set_colouring(col)
+        for s in ("sorted", "atomic", "colour"):
+            got = plan.assemble(K, strategy=s).cpu().numpy()
+            assert got.tobytes() == want.tobytes(), s
+            assert got.sum() == E * m * m
+
+
+@pytest.mark.parametrize("strategy", ["sorted", "atomic", "colour"])
+def test_accumulate_twice_doubles(gpu, orc, strategy):
+    """test_assembly.cpp:89-99: assembling twice without reset doubles every value."""
+    import torch
+    conn, nn, ed, n_rows = problem("quad4", 3, 2, None)
+    E, m = ed.shape
+    K = torch.ones((E, m, m), dtype=torch.float64, device="cuda")
+    with gpu.Plan(ed, n_rows, dofs_per_node=2) as plan:
+        plan.set_colouring(plan.greedy_colouring()[0])
+        v = plan.assemble(K, strategy=strategy)
+        once = v.clone()
+        plan.assemble(K, v, strategy=strategy, accumulate=True)
+        assert torch.equal(v, 2 * once)
+
+
+def test_accumulate_is_left_fold_from_existing(gpu, orc):
+    """FEA_ACCUMULATE on the sorted route continues the fold from the slot's value,
+    exactly like assemble_sequential on a non-reset target."""
+    import torch
+    conn, nn, ed, n_rows = problem("hex8", 3, 3, "elements")
+    P = orc.Pattern.build(conn, nn, 3)
+    Kh = orc.fill_k(5, conn.shape[0], ed.shape[1])
+    start = orc.fill_k(9, 1, int(np.ceil(np.sqrt(P.nnz))))[0].reshape(-1)[: P.nnz].copy()
+    want = P.assemble_sequential(ed, Kh, start.copy())
+    with gpu.Plan(ed, n_rows, dofs_per_node=3) as plan:
+        v = torch.from_numpy(start.copy()).cuda()
+        plan.assemble(torch.from_numpy(Kh).cuda(), v, strategy="sorted", accumulate=True)
+        assert v.cpu().numpy().tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("fmt", ["csr", "crac"])
+def test_external_pattern_superset(gpu, orc, fmt):
+    """A caller's pattern with extra entries (random_pattern-style superset): slots resolved
+    by the device CSR search / CRAC Listing-1 search; values bit-exact vs sequential."""
+    import torch
+    conn, nn, ed, n_rows = problem("quad4", 4, 2, "nodes")
+    P = orc.Pattern.build(conn, nn, 2)
+    rp, cs = P.arrays()
+    rng = np.random.default_rng(3)
+    rows = []
+    for r in range(n_rows):
+        extra = rng.choice(n_rows, size=3, replace=False)
+        rows.append(np.unique(np.concatenate([cs[rp[r]:rp[r + 1]], extra])))
+    srp = np.concatenate([[0], np.cumsum([len(x) for x in rows])]).astype(np.int64)
+    scs = np.concatenate(rows).astype(np.int64)
+    S = orc.Pattern.from_arrays(srp, scs)
+    Kh = orc.fill_k(1, conn.shape[0], ed.shape[1])
+    want = S.assemble_sequential(ed, Kh)
+    if fmt == "csr":
+        plan = gpu.Plan.with_pattern(ed, n_rows, srp, scs, "csr")
+    else:
+        cp, ca = S.crac()
+        plan = gpu.Plan.with_pattern(ed, n_rows, cp, ca, "crac")
+    with plan:
+        assert plan.nnz == S.nnz and plan.missing_entry() is None
+        got = plan.assemble(torch.from_numpy(Kh).cuda(), strategy="sorted").cpu().numpy()
+        assert got.tobytes() == want.tobytes()
+        got_a = plan.assemble(torch.from_numpy(Kh).cuda(), strategy="atomic").cpu().numpy()
+        assert close(got_a, want)
+
+
+def test_missing_entry_is_assembly_error(gpu, orc):
+    """test_assembly.cpp:122-141: pattern of the first element only, all four assembled."""
+    import torch
+    conn, nn = M.quad4_structured(2)
+    ed = M.element_dofs(conn, 1)
+    P = orc.Pattern.build(conn[:1], nn, 1)
+    rp, cs = P.arrays()
+    with gpu.Plan.with_pattern(ed, nn, rp, cs, "csr") as plan:
+        miss = plan.missing_entry()
+        assert miss is not None and miss[0] == 1
+        with pytest.raises(gpu.AssemblyError, match="element 1"):
+            plan.assemble(torch.ones((4, 4, 4), dtype=torch.float64, device="cuda"))
+    with pytest.raises(orc.MissingEntry) as ei:
+        P.assemble_sequential(ed, np.ones((4, 4, 4)))
+    assert ei.value.args[0] == miss
+
+
+def test_invalid_colouring_rejected(gpu):
+    """test_assembly.cpp:329-348: a single-colour colouring of a 2x2 mesh conflicts."""
+    conn, nn = M.quad4_structured(2)
+    with gpu.Plan(M.element_dofs(conn, 1), nn) as plan:
+        with pytest.raises(gpu.AssemblyError, match="share dof"):
+            plan.set_colouring(np.zeros(4, np.int32))
+
+
+@pytest.mark.parametrize("k_compact", [False, True])
+def test_row_partition_blocks_concatenate(gpu, orc, k_compact):
+    """Row-partitioned plans: each owned block's CSR/CRAC/values equal the matching slice
+    of the whole-matrix result."""
+    import torch
+    conn, nn, ed, n_rows = problem("hex8", 4, 3, "elements")
+    P = orc.Pattern.build(conn, nn, 3)
+    rp, cs = P.arrays()
+    Kh = orc.fill_k(42, conn.shape[0], ed.shape[1])
+    want = P.assemble_sequential(ed, Kh)
+    cuts = [0, 3 * 40, 3 * 41, 3 * 90, n_rows]
+    for rb, re in zip(cuts[:-1], cuts[1:]):
+        with gpu.Plan(ed, n_rows, dofs_per_node=3, row_range=(rb, re), k_compact=k_compact) as plan:
+            prp, pcs = plan.csr()
+            assert np.array_equal(prp, rp[rb:re + 1] - rp[rb])
+            assert np.array_equal(pcs, cs[rp[rb]:rp[re]])
+            ids = plan.elements()
+            Kp = torch.from_numpy(Kh[ids] if k_compact else Kh).cuda()
+            for s in ("sorted", "atomic"):
+                got = plan.assemble(Kp, strategy=s).cpu().numpy()
+                sl = want[rp[rb]:rp[re]]
+                if s == "sorted":
+                    assert got.tobytes() == sl.tobytes()
+                else:
+                    assert close(got, sl)
+
+
+def test_host_end_to_end(gpu, orc):
+    conn, nn, ed, n_rows = problem("hex8", 3, 3, "elements")
+    P = orc.Pattern.build(conn, nn, 3)
+    Kh = orc.fill_k(42, conn.shape[0], ed.shape[1])
+    want = P.assemble_sequential(ed, Kh)
+    with gpu.Plan(ed, n_rows, dofs_per_node=3) as plan:
+        got = plan.assemble_host(Kh, strategy="sorted")
+        assert got.tobytes() == want.tobytes()
+
+
+def test_empty_and_degenerate(gpu):
+    """test_formats.cpp:111-139: empty pattern / empty rows."""
+    import torch
+    ed = np.zeros((0, 4), np.int64)
+    with gpu.Plan(ed, 0) as plan:
+        assert (plan.n_rows, plan.nnz, plan.n_runs) == (0, 0, 0)
+        rp, ca = plan.crac()
+        assert list(rp) == [0] and list(ca) == [0, 0]
+    # rows with no element (isolated DOFs 4..7)
+    conn, nn = M.quad4_structured(1)
+    with gpu.Plan(M.element_dofs(conn, 1), 8) as plan:
+        rp, cs = plan.csr()
+        assert list(rp[4:]) == [16, 16, 16, 16, 16]
+        v = plan.assemble(torch.ones((1, 4, 4), dtype=torch.float64, device="cuda"))
+        assert torch.all(v == 1.0)
