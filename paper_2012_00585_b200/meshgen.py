@@ -44,13 +44,18 @@ def quad4_structured(n: int):
     return conn, nv * nv
 
 
-def hex8_structured(n: int):
-    nv = n + 1
-    z, y, x = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
-    base = ((z * nv + y) * nv + x).reshape(-1)
-    ex, ey, ez = 1, nv, nv * nv
+def hex8_box(nx: int, ny: int, nz: int):
+    """nx x ny x nz hex8 elements; node (x,y,z) = (z*(ny+1)+y)*(nx+1)+x."""
+    ax, ay = nx + 1, ny + 1
+    z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    base = ((z * ay + y) * ax + x).reshape(-1).astype(np.int64)
+    ex, ey, ez = 1, ax, ax * ay
     offs = np.array([0, ex, ex + ey, ey, ez, ez + ex, ez + ex + ey, ez + ey], dtype=np.int64)
-    return (base[:, None] + offs[None, :]).astype(np.int64), nv ** 3
+    return base[:, None] + offs[None, :], ax * ay * (nz + 1)
+
+
+def hex8_structured(n: int):
+    return hex8_box(n, n, n)
 
 
 _KUHN_PERMS = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]
