@@ -104,6 +104,7 @@ struct fea_plan {
     int64_t miss_e = -1, miss_r = -1, miss_c = -1;
     // bookkeeping
     int32_t last_launches = 0;
+    bool tma_disabled = false;            // FEA_GATHER_NO_TMA=1: register-staged gather (A/B)
     feagpu::DevBuf stage_K, stage_V;       // fea_assemble_host staging
     int64_t kbytes_required() const;
     int64_t krows() const { return k_compact ? E : E_in; }

@@ -38,17 +38,94 @@ unsigned grid_for(int64_t n, int threads) {
 
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 
+// --- TMA bulk copy + mbarrier primitives (sm_90+/sm_100a PTX) ---------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(bar),
+        "r"(phase)
+        : "memory");
+}
+// 1D bulk copy global -> shared (TMA, SASS UBLKCP), completion via mbarrier tx bytes;
+// L2 evict-first: each K byte is read exactly once.
+__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes,
+                                            uint32_t bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// Ampere-style async copy global -> shared (SASS LDGSTS), 8 or 16 bytes per lane,
+// bypassing registers; completion tracked by an mbarrier (cp.async.mbarrier.arrive).
+template <int UNIT>
+__device__ __forceinline__ void cp_async(uint32_t dst, uint64_t src) {
+    if constexpr (UNIT == 16)
+        asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------
 // Deterministic owner-computes gather (sort-by-slot segmented reduction)
 // ---------------------------------------------------------------------------
-// G lanes per node; R rounds of G entries cover one d*m chunk; PF chunks are
-// in flight per group (register double-buffering for memory parallelism).
+// A group of G lanes owns one node: the node's d rows are one contiguous block of
+// values. The group streams the node's incident element-matrix row blocks
+// K[e][a*d..a*d+d-1][:] (d*m contiguous doubles each, one per incident element,
+// ascending element id) straight into registers — R rounds of G entries per
+// block, PF blocks in flight — and folds them into a shared-memory copy of the
+// node block (one __syncwarp between blocks), then writes the block once with
+// coalesced streaming stores. Per slot this is a left fold from the slot's
+// start value in ascending element order: bit-identical to assemble_sequential
+// (assembly.hpp:112-118). K is read once, values written once, no atomics.
+// The node's incidence list and position-map slice are loaded once per node
+// (coalesced, into registers / shared memory) so no dependent global load sits
+// between two row-block loads. Kept lean in registers: occupancy (many warps,
+// each with a few KB in flight) is what saturates HBM on this random-block gather.
 template <int G, int R, int PF, class PosT>
 __global__ void __launch_bounds__(kWarps * 32)
     k_gather(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
              const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
              const int64_t* __restrict__ nptr, int64_t n_own, int d, int npe, int acc_stride,
-             int accumulate, double* __restrict__ values) {
+             int pos_stride, int accumulate, double* __restrict__ values) {
     extern __shared__ double sacc[];
     constexpr int GPW = 32 / G;
     const int m = d * npe;
@@ -57,33 +134,42 @@ __global__ void __launch_bounds__(kWarps * 32)
     const int gl = lane % G;
     const int gw = lane / G;
     const int warp = threadIdx.x >> 5;
-    double* acc = sacc + static_cast<int64_t>(warp * GPW + gw) * acc_stride;
+    const int grp = warp * GPW + gw;
+    double* acc = sacc + static_cast<int64_t>(grp) * acc_stride;
+    PosT* spos = reinterpret_cast<PosT*>(sacc + static_cast<int64_t>(kWarps) * GPW * acc_stride) +
+                 static_cast<int64_t>(grp) * pos_stride;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
 
-    // chunk-independent decode of this lane's entries: idx -> (ki, b, kj)
-    int t_ki[R], t_b[R], t_kj[R];
+    // chunk-independent decode of this lane's entries, packed ki | b<<10 | kj<<20
+    uint32_t tab[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int idx = r * G + gl;
         const int ki = idx / m;
         const int j = idx - ki * m;
         const int b = j / d;
-        t_ki[r] = ki;
-        t_b[r] = idx < dm ? b : 0;
-        t_kj[r] = j - b * d;
+        tab[r] = idx < dm ? (static_cast<uint32_t>(ki) | (static_cast<uint32_t>(b) << 10) |
+                             (static_cast<uint32_t>(j - b * d) << 20))
+                          : 0u;
     }
 
     const int64_t v = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * GPW + gw;
-    const bool active = v < n_own;
-    int64_t b0 = 0;
+    int64_t b0 = 0, vb = 0;
     int n = 0, rowlen = 0, block = 0;
-    int64_t vb = 0;
-    if (active) {
+    if (v < n_own) {
         b0 = adj_ptr[v];
         n = static_cast<int>(adj_ptr[v + 1] - b0);
-        const int64_t cnt = nptr[v + 1] - nptr[v];
-        rowlen = static_cast<int>(d * cnt);
+        const int64_t c0 = nptr[v];
+        rowlen = static_cast<int>(d * (nptr[v + 1] - c0));
         block = d * rowlen;
-        vb = static_cast<int64_t>(d) * d * nptr[v];
+        vb = static_cast<int64_t>(d) * d * c0;
+    }
+    // the node's incidences (lane gl holds entry gl when n <= G) and position slice
+    const int32_t my_ent = gl < n ? adj[b0 + gl] : 0;
+    {
+        const int np = n * npe;
+        const PosT* src = posA + b0 * npe;
+        for (int q = gl; q < np; q += G) spos[q] = src[q];
     }
     if (accumulate) {
         for (int i = gl; i < block; i += G) acc[i] = values[vb + i];
@@ -94,42 +180,46 @@ __global__ void __launch_bounds__(kWarps * 32)
     __syncwarp();
 
     double kv[PF][R];
-    PosT pv[PF][R];
+    auto entry_of = [&](int k) -> int32_t {
+        const int32_t e = __shfl_sync(0xffffffffu, my_ent, (gw * G + (k & (G - 1))) & 31);
+        return n <= G ? e : (k < n ? adj[b0 + k] : 0);
+    };
     auto load = [&](int p, int k) {
-        const int32_t entry = adj[b0 + k];
-        const double* src = K + static_cast<int64_t>(entry) * dm;
-        const PosT* ps = posA + (b0 + k) * npe;
+        const int32_t entry = entry_of(k);
+        if (k < n) {
+            const double* src = K + static_cast<int64_t>(entry) * dm;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int idx = r * G + gl;
-            if (idx < dm) {
-                kv[p][r] = ld_stream(src + idx);
-                pv[p][r] = ps[t_b[r]];
+            for (int r = 0; r < R; ++r) {
+                const int idx = r * G + gl;
+                if (idx < dm) kv[p][r] = ld_stream(src + idx);
             }
         }
     };
 #pragma unroll
-    for (int p = 0; p < PF; ++p)
-        if (p < n) load(p, p);
+    for (int p = 0; p < PF; ++p) load(p, p);
 
     for (int k0 = 0; k0 < n_max; k0 += PF) {
 #pragma unroll
         for (int p = 0; p < PF; ++p) {
             const int k = k0 + p;
             if (k < n) {
+                const PosT* pk = spos + k * npe;
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const int idx = r * G + gl;
                     if (idx < dm) {
-                        const int s = t_ki[r] * rowlen + static_cast<int>(pv[p][r]) * d + t_kj[r];
-                        acc[s] += kv[p][r];
+                        const uint32_t t = tab[r];
+                        const int q = static_cast<int>(t & 1023u) * rowlen +
+                                      static_cast<int>(pk[(t >> 10) & 1023u]) * d + static_cast<int>(t >> 20);
+                        acc[q] += kv[p][r];
                     }
                 }
             }
             __syncwarp();
-            if (k + PF < n) load(p, k + PF);
+            load(p, k + PF);
         }
     }
+    (void)gmask;
     for (int i = gl; i < block; i += G) __stcs(values + vb + i, acc[i]);
 }
 
@@ -296,7 +386,9 @@ template <int G, int R, int PF, class PosT>
 void run_gather(fea_plan* p, const double* K, double* values, bool accumulate, cudaStream_t s) {
     constexpr int GPW = 32 / G;
     const int acc_stride = p->d * p->d * p->max_cnt + 1;  // +1 staggers groups across banks
-    size_t smem = static_cast<size_t>(kWarps) * GPW * acc_stride * sizeof(double);
+    const int pos_stride = static_cast<int>((std::max<int64_t>(p->max_adj, 1) * p->npe + 7) & ~int64_t(7));
+    size_t smem = static_cast<size_t>(kWarps) * GPW *
+                  (acc_stride * sizeof(double) + pos_stride * sizeof(PosT));
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID,
                 "node row block too large for shared-memory accumulation");
     auto kern = k_gather<G, R, PF, PosT>;
@@ -307,7 +399,8 @@ void run_gather(fea_plan* p, const double* K, double* values, bool accumulate, c
     if (blocks == 0) return;
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
         K, p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->posA.as<PosT>(),
-        p->nptr.as<int64_t>(), p->n_own, p->d, p->npe, acc_stride, accumulate ? 1 : 0, values);
+        p->nptr.as<int64_t>(), p->n_own, p->d, p->npe, acc_stride, pos_stride,
+        accumulate ? 1 : 0, values);
     FEA_CK(cudaGetLastError());
     p->last_launches += 1;
 }

@@ -20,6 +20,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -536,7 +537,7 @@ void build_adjacency(fea_plan* p, cudaStream_t s) {
     FEA_CK(cudaMemcpyAsync(&p->n_adj, p->adj_ptr.as<int64_t>() + p->n_own, sizeof(int64_t),
                            cudaMemcpyDeviceToHost, s));
     FEA_CK(cudaStreamSynchronize(s));
-    p->adj.alloc(p->n_adj * 4);
+    p->adj.alloc(p->n_adj * 4 + 64);  // slack: 16B-rounded bulk copies of adjacency slices
     if (p->n_adj > 0)
         FEA_CK(cudaMemcpyAsync(p->adj.p, vals_out.p, p->n_adj * 4, cudaMemcpyDeviceToDevice, s));
     // largest node incidence count (reporting / sizing)
@@ -653,7 +654,7 @@ void build_own_pattern(fea_plan* p, cudaStream_t s) {
             big.as<int32_t>(), nullptr, p->nptr.as<int64_t>(), p->ncol.as<int32_t>());
     FEA_CK(cudaGetLastError());
     // slot map (adjacency order)
-    p->posA.alloc(p->n_adj * p->npe * p->pos_bytes);
+    p->posA.alloc(p->n_adj * p->npe * p->pos_bytes + 64);  // slack: 16B-rounded bulk copies
     if (p->n_own > 0) {
         if (p->pos_bytes == 1)
             k_pos_adj<uint8_t><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
@@ -834,6 +835,7 @@ fea_status fea_plan_create(int device, const int64_t* elem_dofs, int64_t n_eleme
         Stream st;
         auto p = std::make_unique<fea_plan>();
         p->device = device;
+        p->tma_disabled = std::getenv("FEA_GATHER_NO_TMA") != nullptr;
         p->E_in = n_elements;
         p->m = m;
         p->n_rows = n_rows;
@@ -943,7 +945,7 @@ fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, in
         }
         miss.alloc(8);
         FEA_CK(cudaMemsetAsync(miss.p, 0xff, 8, s));
-        p->posA.alloc(p->n_adj * p->npe * p->pos_bytes);
+        p->posA.alloc(p->n_adj * p->npe * p->pos_bytes + 64);
         const unsigned blocks = grid_for(n_rows * 32, 256);
         if (n_rows > 0) {
 #define FEA_LAUNCH_EXT(T, C)                                                                   \
