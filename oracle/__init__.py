@@ -294,3 +294,24 @@ class RefProblem:
 
 def hardware_threads() -> int:
     return int(ref().ref_hardware_threads())
+
+
+def ref_structured_element_nodes(n: int, p: int, d: int = 1):
+    """(element_nodes (E, (p+1)^2), n_nodes) from the reference's build_dof_map(generate_structured(n), p, d)."""
+    L = ref()
+    L.ref_structured_element_nodes.restype = c_int
+    L.ref_structured_element_nodes.argtypes = [c_int64, c_int, c_int, c_void_p, POINTER(c_int64),
+                                               POINTER(c_int64), POINTER(c_int64)]
+    E, npe, nn = c_int64(), c_int64(), c_int64()
+    if L.ref_structured_element_nodes(n, p, d, c_void_p(0), ctypes.byref(E), ctypes.byref(npe), ctypes.byref(nn)):
+        raise RuntimeError(L.ref_last_error().decode())
+    out = np.empty((E.value, npe.value), np.int64)
+    L.ref_structured_element_nodes(n, p, d, _p(out), ctypes.byref(E), ctypes.byref(npe), ctypes.byref(nn))
+    return out, nn.value
+
+
+def ref_speed_factor(t_seq: float, t_method: float) -> float:
+    L = ref()
+    L.ref_speed_factor.restype = c_double
+    L.ref_speed_factor.argtypes = [c_double, c_double]
+    return float(L.ref_speed_factor(t_seq, t_method))

@@ -269,3 +269,26 @@ extern "C" int ref_assemble(void* h, const double* K, int method, int format, in
         return 3;
     }
 }
+
+// The reference's own 2D meshes and DOF numbering (mesh.cpp:62-85, dof_map.cpp:24-67):
+// element node lists of build_dof_map(generate_structured(n), p, d). Call with
+// out == nullptr to get the sizes.
+extern "C" int ref_structured_element_nodes(int64_t n, int p, int d, int64_t* out,
+                                            int64_t* n_elements, int64_t* npe, int64_t* n_nodes) {
+    try {
+        const fea::DofMap map = fea::build_dof_map(fea::generate_structured(n), p, d);
+        *n_elements = map.n_elements;
+        *npe = map.nodes_per_element();
+        *n_nodes = map.n_nodes;
+        if (out) std::memcpy(out, map.element_nodes.data(), map.element_nodes.size() * 8);
+        return 0;
+    } catch (const std::exception& ex) {
+        g_err = ex.what();
+        return 1;
+    }
+}
+
+// speed_factor / storage_factor (bench.cpp:93-113) for the golden arithmetic checks.
+extern "C" double ref_speed_factor(double t_seq, double t_method) {
+    return fea::speed_factor(t_seq, t_method);
+}

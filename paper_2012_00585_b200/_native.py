@@ -9,7 +9,9 @@ import ctypes
 from ctypes import POINTER, c_char_p, c_int, c_int32, c_int64, c_uint32, c_uint64, c_void_p
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().with_name("libfea_gpu.so")
+import os
+
+LIB_PATH = Path(os.environ.get("FEA_LIB_PATH") or Path(__file__).resolve().with_name("libfea_gpu.so"))
 
 FEA_OK = 0
 FEA_ERR_INVALID = 1

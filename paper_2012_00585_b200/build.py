@@ -29,16 +29,19 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
+def build(verbose: bool = False, force: bool = False, out: Path | None = None,
+          defines: tuple[str, ...] = ()) -> Path:
+    """Compile the library; `out`/`defines` build tuning variants (e.g. -DFEA_GATHER_MIN_BLOCKS=5)."""
+    lib = LIB if out is None else Path(out)
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "fea_gpu.h"]
-    if not force and not _stale(LIB, deps):
-        return LIB
-    objdir = PKG / "_build"
+    if not force and not _stale(lib, deps):
+        return lib
+    objdir = PKG / ("_build" if out is None else "_build_" + lib.stem)
     objdir.mkdir(exist_ok=True)
     objs = []
     for s in SOURCES:
         obj = objdir / (Path(s).stem + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(CSRC / s), "-o", str(obj)]
+        cmd = [NVCC, *ARCH, *FLAGS, *defines, "-c", str(CSRC / s), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
@@ -47,14 +50,14 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             sys.stderr.write(r.stderr)
         (objdir / (Path(s).stem + ".ptxas.txt")).write_text(r.stderr)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

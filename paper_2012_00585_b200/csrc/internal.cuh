@@ -76,6 +76,7 @@ struct fea_plan {
     bool partitioned = false;
     bool k_compact = false;
     bool external = false;   // pattern supplied by the caller
+    bool dup_nodes = false;  // some element lists a node twice (serialised fold variant)
     // sizes
     int64_t n_adj = 0;       // owned (node, element) incidences
     int64_t nnz_nodes = 0;   // node-level pattern entries

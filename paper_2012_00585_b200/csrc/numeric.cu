@@ -120,8 +120,11 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // (coalesced, into registers / shared memory) so no dependent global load sits
 // between two row-block loads. Kept lean in registers: occupancy (many warps,
 // each with a few KB in flight) is what saturates HBM on this random-block gather.
-template <int G, int R, int PF, class PosT>
-__global__ void __launch_bounds__(kWarps * 32)
+#ifndef FEA_GATHER_MIN_BLOCKS
+#define FEA_GATHER_MIN_BLOCKS 5
+#endif
+template <int G, int R, int PF, class PosT, bool DISTINCT>
+__global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
     k_gather(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
              const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
              const int64_t* __restrict__ nptr, int64_t n_own, int d, int npe, int acc_stride,
@@ -204,15 +207,27 @@ __global__ void __launch_bounds__(kWarps * 32)
             const int k = k0 + p;
             if (k < n) {
                 const PosT* pk = spos + k * npe;
+                int q[R];
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    const int idx = r * G + gl;
-                    if (idx < dm) {
-                        const uint32_t t = tab[r];
-                        const int q = static_cast<int>(t & 1023u) * rowlen +
-                                      static_cast<int>(pk[(t >> 10) & 1023u]) * d + static_cast<int>(t >> 20);
-                        acc[q] += kv[p][r];
-                    }
+                    const uint32_t t = tab[r];
+                    q[r] = static_cast<int>(t & 1023u) * rowlen +
+                           static_cast<int>(pk[(t >> 10) & 1023u]) * d + static_cast<int>(t >> 20);
+                }
+                if (DISTINCT) {
+                    // the slots of one element row block are distinct (no repeated node in
+                    // an element): all loads, then all adds, then all stores
+                    double a[R];
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (r * G + gl < dm) a[r] = acc[q[r]];
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (r * G + gl < dm) acc[q[r]] = a[r] + kv[p][r];
+                } else {
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (r * G + gl < dm) acc[q[r]] += kv[p][r];
                 }
             }
             __syncwarp();
@@ -391,7 +406,7 @@ void run_gather(fea_plan* p, const double* K, double* values, bool accumulate, c
                   (acc_stride * sizeof(double) + pos_stride * sizeof(PosT));
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID,
                 "node row block too large for shared-memory accumulation");
-    auto kern = k_gather<G, R, PF, PosT>;
+    auto kern = p->dup_nodes ? k_gather<G, R, PF, PosT, false> : k_gather<G, R, PF, PosT, true>;
     if (smem > 48 * 1024)
         FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t groups = p->n_own;

@@ -122,6 +122,10 @@ __global__ void k_extract_conn(const int64_t* __restrict__ dofs, int64_t total, 
                 if (x < 0 || x >= n_rows) f |= 2u;
             }
         }
+        // a node repeated inside one element (bit 2): the reference adds both
+        // occurrences in order; the gather then keeps a serialised fold
+        for (int b = 0; b < a; ++b)
+            if (dofs[e * m + (int64_t)b * d] == base) f |= 4u;
         if (f) atomicOr(flags, f);
         conn[t] = static_cast<int32_t>(base / d);
     }
@@ -698,6 +702,7 @@ void build_elements(fea_plan* p, const int64_t* elem_dofs, int32_t d_hint, cudaS
         }
         p->d = d;
         p->npe = npe;
+        p->dup_nodes = (h & 4u) != 0;
         break;
     }
     FEA_REQUIRE(p->row_begin % p->d == 0 && p->row_end % p->d == 0, FEA_ERR_INVALID,

@@ -1,0 +1,68 @@
+"""Row-partitioned multi-GPU assembly: ownership, element filtering, optional row-block gather.
+
+SURVEY.md §8e: each rank owns a contiguous range of node rows; it keeps the elements with at
+least one node in its range (the plan does that on the device), assembles its row block with
+no collective, and the row blocks can optionally be gathered to one rank over NCCL. There is
+no reference counterpart (the reference is shared-memory only); this module is the
+host side of that B200 extension and works with any torch.distributed backend (NCCL on GPUs,
+gloo on CPU for the tests).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def owned_node_range(n_nodes: int, world: int, rank: int, weights=None):
+    """Contiguous node range of `rank`: equal node counts, or balanced by `weights`
+    (e.g. node-level NNZ) at the weight quantiles."""
+    if weights is None:
+        return n_nodes * rank // world, n_nodes * (rank + 1) // world
+    c = np.concatenate([[0], np.cumsum(np.asarray(weights, dtype=np.float64))])
+    total = c[-1]
+    cut = lambda r: int(np.searchsorted(c, total * r / world, side="left"))  # noqa: E731
+    lo = 0 if rank == 0 else cut(rank)
+    hi = n_nodes if rank == world - 1 else cut(rank + 1)
+    return lo, hi
+
+
+def owned_row_range(n_nodes: int, d: int, world: int, rank: int, weights=None):
+    lo, hi = owned_node_range(n_nodes, world, rank, weights)
+    return lo * d, hi * d
+
+
+def kept_elements(conn: np.ndarray, node_lo: int, node_hi: int) -> np.ndarray:
+    """Ids (ascending) of the elements with at least one node in [node_lo, node_hi) — the
+    host mirror of the plan's device-side element filter."""
+    own = (conn >= node_lo) & (conn < node_hi)
+    return np.nonzero(own.any(axis=1))[0].astype(np.int64)
+
+
+def redundant_fraction(conn: np.ndarray, n_nodes: int, world: int) -> float:
+    """Extra element work of row partitioning: sum of kept elements over ranks / E - 1."""
+    total = 0
+    for r in range(world):
+        lo, hi = owned_node_range(n_nodes, world, r)
+        total += len(kept_elements(conn, lo, hi))
+    return total / conn.shape[0] - 1.0
+
+
+def gather_row_blocks(values_local, root: int = 0, group=None):
+    """Gather every rank's row block of values (1-D, any length) to `root`, concatenated in
+    rank order (= global row order for contiguous ownership). Returns the full values array on
+    `root` and None elsewhere. Lengths are exchanged first, so blocks may differ in size."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n = torch.tensor([values_local.numel()], dtype=torch.int64, device=values_local.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    mx = max(sizes)
+    buf = torch.zeros(mx, dtype=values_local.dtype, device=values_local.device)
+    buf[: values_local.numel()] = values_local
+    out = [torch.empty_like(buf) for _ in range(world)] if rank == root else None
+    dist.gather(buf, out, dst=root, group=group)
+    if rank != root:
+        return None
+    return torch.cat([o[:s] for o, s in zip(out, sizes)])
