@@ -35,6 +35,12 @@
 extern "C" {
 #endif
 
+#if defined(__GNUC__)
+#define FEA_API __attribute__((visibility("default")))
+#else
+#define FEA_API
+#endif
+
 typedef enum {
     FEA_OK = 0,
     FEA_ERR_INVALID = 1,        /* std::invalid_argument / std::out_of_range (dof_map.cpp:25-27, :82-84) */
@@ -76,10 +82,10 @@ typedef enum {
 typedef struct fea_plan fea_plan;
 
 /* Message of the last failure on this thread ("" if none). */
-const char* fea_last_error(void);
+FEA_API const char* fea_last_error(void);
 
 /* Library/ABI version: major*10000 + minor*100 + patch. */
-int fea_version(void);
+FEA_API int fea_version(void);
 
 /*
  * Symbolic phase + slot-map build.
@@ -95,7 +101,7 @@ int fea_version(void);
  *                whole matrix is [0, n_rows). Only owned rows are assembled; the
  *                plan's CSR/CRAC row block is rebased to 0, columns stay global.
  */
-fea_status fea_plan_create(int device, const int64_t* elem_dofs, int64_t n_elements, int32_t m,
+FEA_API fea_status fea_plan_create(int device, const int64_t* elem_dofs, int64_t n_elements, int32_t m,
                            int64_t n_rows, int32_t dofs_per_node, int64_t row_begin,
                            int64_t row_end, uint32_t flags, fea_plan** out);
 
@@ -110,45 +116,45 @@ fea_status fea_plan_create(int device, const int64_t* elem_dofs, int64_t n_eleme
  *  format FEA_FORMAT_CSR : row_ptr[n_rows+1], idx = cols[nnz]
  *  format FEA_FORMAT_CRAC: row_ptr[n_rows+1] in col_align entry units, idx = col_align[2*runs+2]
  */
-fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, int64_t n_elements,
+FEA_API fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, int64_t n_elements,
                                         int32_t m, int64_t n_rows, int32_t format,
                                         const int64_t* row_ptr, const int64_t* idx,
                                         fea_plan** out);
 
-void fea_plan_destroy(fea_plan* plan);
+FEA_API void fea_plan_destroy(fea_plan* plan);
 
 /* Sizes of the plan's (owned) row block: rows, nnz (= values length), CRAC runs
  * (count_pattern_runs, pattern.cpp:110-120), kept elements. */
-fea_status fea_plan_sizes(const fea_plan* plan, int64_t* n_rows, int64_t* nnz, int64_t* n_runs,
+FEA_API fea_status fea_plan_sizes(const fea_plan* plan, int64_t* n_rows, int64_t* nnz, int64_t* n_runs,
                           int64_t* n_elements);
 
 /* Slot-map / plan details for reporting: dofs per node used, nodes per element,
  * bytes of device metadata held by the plan. */
-fea_status fea_plan_info(const fea_plan* plan, int32_t* dofs_per_node, int32_t* nodes_per_element,
+FEA_API fea_status fea_plan_info(const fea_plan* plan, int32_t* dofs_per_node, int32_t* nodes_per_element,
                          int64_t* metadata_bytes);
 
 /* CSR arrays of the plan (SparsityPattern::row_ptr/cols, pattern.hpp:29-35):
  * row_ptr[n_rows+1], cols[nnz]; host or device destinations. */
-fea_status fea_plan_copy_csr(const fea_plan* plan, int64_t* row_ptr, int64_t* cols);
+FEA_API fea_status fea_plan_copy_csr(const fea_plan* plan, int64_t* row_ptr, int64_t* cols);
 
 /* CRAC arrays (CracBase::rows / col_align, formats.hpp:257-273): row_ptr[n_rows+1]
  * in col_align entry units, col_align[2*runs+2] with the final (0, nnz) pair. */
-fea_status fea_plan_copy_crac(const fea_plan* plan, int64_t* row_ptr, int64_t* col_align);
+FEA_API fea_status fea_plan_copy_crac(const fea_plan* plan, int64_t* row_ptr, int64_t* col_align);
 
 /* Ids (ascending) of the elements the plan keeps (those with a node in the owned
  * row range); elem_ids[n_elements] from fea_plan_sizes. */
-fea_status fea_plan_copy_elements(const fea_plan* plan, int64_t* elem_ids);
+FEA_API fea_status fea_plan_copy_elements(const fea_plan* plan, int64_t* elem_ids);
 
 /* Greedy colouring of the plan's elements — fea::greedy_colouring
  * (colouring.cpp:24-75): ascending element order, smallest colour unused by any
  * node-sharing element. colour_of[E] (host). */
-fea_status fea_plan_greedy_colouring(const fea_plan* plan, int32_t* colour_of, int32_t* n_colours);
+FEA_API fea_status fea_plan_greedy_colouring(const fea_plan* plan, int32_t* colour_of, int32_t* n_colours);
 
 /* Install the colouring used by FEA_DET_COLOUR (Colouring::colour_of,
  * colouring.hpp:35-39; host array over all E input elements). Validated like
  * find_colour_conflict (colouring.cpp:91-119): two same-colour elements sharing
  * a DOF -> FEA_ERR_INVALID_COLOURING. */
-fea_status fea_plan_set_colouring(fea_plan* plan, const int32_t* colour_of);
+FEA_API fea_status fea_plan_set_colouring(fea_plan* plan, const int32_t* colour_of);
 
 /*
  * Numeric phase.
@@ -160,29 +166,29 @@ fea_status fea_plan_set_colouring(fea_plan* plan, const int32_t* colour_of);
  *  flags   FEA_ACCUMULATE or FEA_OVERWRITE
  *  stream  cudaStream_t (as void*)
  */
-fea_status fea_assemble(fea_plan* plan, const double* K, int32_t strategy, double* values,
+FEA_API fea_status fea_assemble(fea_plan* plan, const double* K, int32_t strategy, double* values,
                         uint32_t flags, void* stream);
 
 /* End-to-end form with HOST buffers (pinned or pageable): copies K host->device,
  * assembles, copies values device->host; synchronous like the reference call
  * (SPEC.md:364). Device staging buffers are cached in the plan. */
-fea_status fea_assemble_host(fea_plan* plan, const double* K_host, int32_t strategy,
+FEA_API fea_status fea_assemble_host(fea_plan* plan, const double* K_host, int32_t strategy,
                              double* values_host, uint32_t flags, void* stream);
 
 /* The missing entry behind FEA_ERR_MISSING_ENTRY: element, row, column (the
  * values AssemblyError names, assembly.hpp:65-73). Returns FEA_OK with e = -1
  * when the plan has none. */
-fea_status fea_plan_missing_entry(const fea_plan* plan, int64_t* element, int64_t* row,
+FEA_API fea_status fea_plan_missing_entry(const fea_plan* plan, int64_t* element, int64_t* row,
                                   int64_t* col);
 
 /* Number of kernel launches the last fea_assemble issued on this plan. */
-int32_t fea_plan_last_launches(const fea_plan* plan);
+FEA_API int32_t fea_plan_last_launches(const fea_plan* plan);
 
 /* Seeded synthetic element matrices: K[i][r][c] = U(seed, id_i, min(r,c), max(r,c)),
  * symmetric, uniform on [-1,1), exactly representable (the counter-hash supplier of
  * SURVEY.md §7.2; stands in for ElementMatrixSupplier, assembly.hpp:37).
  * elem_ids: NULL (id_i = i) or device int64[n]. */
-fea_status fea_fill_seeded_k(double* K, int64_t n, int32_t m, uint64_t seed,
+FEA_API fea_status fea_fill_seeded_k(double* K, int64_t n, int32_t m, uint64_t seed,
                              const int64_t* elem_ids, void* stream);
 
 #ifdef __cplusplus

@@ -18,7 +18,7 @@ LIB = PKG / "libfea_gpu.so"
 SOURCES = ["plan.cu", "numeric.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-fvisibility=hidden", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}"]
 
 
