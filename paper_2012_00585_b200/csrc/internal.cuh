@@ -85,6 +85,7 @@ struct fea_plan {
     int32_t max_cnt = 0;     // longest node-level row
     int64_t max_adj = 0;     // most elements at one node
     int32_t pos_bytes = 1;   // 1 (uint8) or 2 (uint16) row-relative positions
+    int32_t pstride = 0;     // posA entries per incidence: npe rounded up to a 4-byte multiple
     // device metadata
     feagpu::DevBuf conn_k;    // int32 [krows*npe] node ids, indexed by K row
     feagpu::DevBuf elem_id;   // int64 [E] global ids of kept elements, ascending
@@ -105,7 +106,6 @@ struct fea_plan {
     int64_t miss_e = -1, miss_r = -1, miss_c = -1;
     // bookkeeping
     int32_t last_launches = 0;
-    bool tma_disabled = false;            // FEA_GATHER_NO_TMA=1: register-staged gather (A/B)
     feagpu::DevBuf stage_K, stage_V;       // fea_assemble_host staging
     int64_t kbytes_required() const;
     int64_t krows() const { return k_compact ? E : E_in; }

@@ -104,8 +104,14 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+#ifndef FEA_GATHER_MIN_BLOCKS
+#define FEA_GATHER_MIN_BLOCKS 5
+#endif
+#ifndef FEA_GATHER_MIN_BLOCKS_WIDE
+#define FEA_GATHER_MIN_BLOCKS_WIDE 4
+#endif
 // ---------------------------------------------------------------------------
-// Deterministic owner-computes gather (sort-by-slot segmented reduction)
+// Deterministic owner-computes gather, one node per lane group (FEA_DET_SORTED)
 // ---------------------------------------------------------------------------
 // A group of G lanes owns one node: the node's d rows are one contiguous block of
 // values. The group streams the node's incident element-matrix row blocks
@@ -120,15 +126,12 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // (coalesced, into registers / shared memory) so no dependent global load sits
 // between two row-block loads. Kept lean in registers: occupancy (many warps,
 // each with a few KB in flight) is what saturates HBM on this random-block gather.
-#ifndef FEA_GATHER_MIN_BLOCKS
-#define FEA_GATHER_MIN_BLOCKS 5
-#endif
 template <int G, int R, int PF, class PosT, bool DISTINCT>
 __global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
-    k_gather(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
+    k_gather_node(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
              const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
-             const int64_t* __restrict__ nptr, int64_t n_own, int d, int npe, int acc_stride,
-             int pos_stride, int accumulate, double* __restrict__ values) {
+             const int64_t* __restrict__ nptr, int64_t n_own, int d, int npe, int pstride,
+             int acc_stride, int pos_stride, int accumulate, double* __restrict__ values) {
     extern __shared__ double sacc[];
     constexpr int GPW = 32 / G;
     const int m = d * npe;
@@ -171,8 +174,10 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
     const int32_t my_ent = gl < n ? adj[b0 + gl] : 0;
     {
         const int np = n * npe;
-        const PosT* src = posA + b0 * npe;
-        for (int q = gl; q < np; q += G) spos[q] = src[q];
+        for (int q = gl; q < np; q += G) {
+            const int k = q / npe;
+            spos[q] = posA[(b0 + k) * pstride + (q - k * npe)];
+        }
     }
     if (accumulate) {
         for (int i = gl; i < block; i += G) acc[i] = values[vb + i];
@@ -236,6 +241,196 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
     }
     (void)gmask;
     for (int i = gl; i < block; i += G) __stcs(values + vb + i, acc[i]);
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic owner-computes gather, persistent streaming form (FEA_DET_SORTED)
+// ---------------------------------------------------------------------------
+// A group of G lanes owns a contiguous range of nodes [va, vb); each node's d rows
+// are one contiguous block of values. Incidence lists of consecutive nodes are
+// contiguous, so the group's work is ONE stream of element-matrix row blocks
+// ("chunks") K[e][a*d..a*d+d-1][:], chunk t = adj[t] for t in
+// [adj_ptr[va], adj_ptr[vb]), segmented by node — a CSR segmented reduction. The
+// group keeps PF chunks in flight in registers (R rounds of G doubles each),
+// continuously across node boundaries. Chunk indices and position-map words are
+// staged through a per-group shared-memory ring: loaded into registers one block
+// (kBlk chunks) early and stored when the block before is finished, so no
+// dependent global load ever sits between two chunk loads. Each chunk is folded
+// into the node's shared accumulator in ascending element order (group-local
+// __syncwarp between chunks: a per-slot left fold from the slot's start value,
+// bit-identical to assemble_sequential, assembly.hpp:112-118); at a node boundary
+// the block is written once with coalesced streaming stores. K is read exactly
+// once, values written once, no atomics.
+constexpr int kPosW = 8;  // max position-map words staged per lane per block
+template <int G>
+constexpr int blk_of() { return G < 16 ? 16 : G; }  // chunks per staging block (>= G)
+
+template <int R>
+constexpr int gather_min_blocks() { return R >= 8 ? FEA_GATHER_MIN_BLOCKS_WIDE : FEA_GATHER_MIN_BLOCKS; }
+
+template <int G, int R, int PF, class PosT, bool DISTINCT>
+__global__ void __launch_bounds__(kWarps * 32, gather_min_blocks<R>())
+    k_gather_stream(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
+             const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
+             const int64_t* __restrict__ nptr, int64_t n_own, int64_t n_groups, int d, int npe,
+             int pstride, int acc_stride, int accumulate, double* __restrict__ values) {
+    extern __shared__ double sacc[];
+    constexpr int GPW = 32 / G;
+    constexpr int kBlk = blk_of<G>();
+    constexpr int EPL = kBlk / G;  // staged chunk indices per lane per block
+    const int m = d * npe;
+    const int dm = d * m;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G;
+    const int gw = lane / G;
+    const int warp = threadIdx.x >> 5;
+    const int grp = warp * GPW + gw;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
+    const int pw_blk = kBlk * pstride * static_cast<int>(sizeof(PosT)) / 4;  // words per block
+    double* acc = sacc + static_cast<int64_t>(grp) * acc_stride;
+    int32_t* ring = reinterpret_cast<int32_t*>(sacc + static_cast<int64_t>(kWarps) * GPW * acc_stride) +
+                    static_cast<int64_t>(grp) * 2 * (kBlk + pw_blk);
+    int32_t* ent_ring = ring;                 // [2][kBlk]
+    uint32_t* pos_ring = reinterpret_cast<uint32_t*>(ring + 2 * kBlk);  // [2][pw_blk] words
+
+    uint32_t tab[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int idx = r * G + gl;
+        const int ki = idx / m;
+        const int j = idx - ki * m;
+        const int b = j / d;
+        tab[r] = idx < dm ? (static_cast<uint32_t>(ki) | (static_cast<uint32_t>(b) << 10) |
+                             (static_cast<uint32_t>(j - b * d) << 20))
+                          : 0u;
+    }
+
+    const int64_t g = (static_cast<int64_t>(blockIdx.x) * kWarps + warp) * GPW + gw;
+    const int64_t va = n_own * g / n_groups;
+    const int64_t vend = n_own * (g + 1) / n_groups;
+    if (va >= vend) return;
+    const int64_t t0 = adj_ptr[va];
+    const int64_t t_end = adj_ptr[vend];
+    const uint32_t* pos_words = reinterpret_cast<const uint32_t*>(posA);
+    const int64_t pw_end = t_end * pstride * static_cast<int64_t>(sizeof(PosT)) / 4;
+
+    int32_t se[EPL];
+    uint32_t sp[kPosW];
+    auto load_block = [&](int64_t blk) {
+        const int64_t tb = t0 + blk * kBlk;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+            const int64_t t = tb + i * G + gl;
+            se[i] = t < t_end ? adj[t] : 0;
+        }
+        const int64_t wb = tb * pstride * static_cast<int64_t>(sizeof(PosT)) / 4;
+#pragma unroll
+        for (int i = 0; i < kPosW; ++i) {
+            const int q = i * G + gl;
+            if (q < pw_blk && wb + q < pw_end) sp[i] = pos_words[wb + q];
+        }
+    };
+    auto store_block = [&](int64_t blk) {
+        const int slot = static_cast<int>(blk & 1);
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) ent_ring[slot * kBlk + i * G + gl] = se[i];
+#pragma unroll
+        for (int i = 0; i < kPosW; ++i) {
+            const int q = i * G + gl;
+            if (q < pw_blk) pos_ring[slot * pw_blk + q] = sp[i];
+        }
+    };
+    load_block(0);
+    store_block(0);
+    load_block(1);
+    store_block(1);
+    load_block(2);
+    __syncwarp(gmask);
+
+    int64_t v = va;
+    int64_t seg_end = adj_ptr[v + 1];
+    int64_t c0 = nptr[v];
+    int rowlen = static_cast<int>(d * (nptr[v + 1] - c0));
+    int block = d * rowlen;
+    int64_t vbase = static_cast<int64_t>(d) * d * c0;
+    for (int i = gl; i < block; i += G) acc[i] = accumulate ? values[vbase + i] : 0.0;
+    __syncwarp(gmask);
+
+    double kv[PF][R];
+    auto issue = [&](int p, int64_t t) {
+        if (t < t_end) {
+            const int32_t e = ent_ring[(t - t0) & (2 * kBlk - 1)];
+            const double* src = K + static_cast<int64_t>(e) * dm;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (r * G + gl < dm) kv[p][r] = ld_stream(src + r * G + gl);
+        }
+    };
+#pragma unroll
+    for (int p = 0; p < PF; ++p) issue(p, t0 + p);
+
+    const PosT* pos_ring_t = reinterpret_cast<const PosT*>(pos_ring);
+    for (int64_t tt = t0; tt < t_end; tt += PF) {
+#pragma unroll
+        for (int p = 0; p < PF; ++p) {
+            const int64_t t = tt + p;
+            if (t < t_end) {
+                while (t >= seg_end) {  // node boundary: write the finished block(s)
+                    for (int i = gl; i < block; i += G) __stcs(values + vbase + i, acc[i]);
+                    ++v;
+                    seg_end = adj_ptr[v + 1];
+                    c0 = nptr[v];
+                    rowlen = static_cast<int>(d * (nptr[v + 1] - c0));
+                    block = d * rowlen;
+                    vbase = static_cast<int64_t>(d) * d * c0;
+                    __syncwarp(gmask);
+                    for (int i = gl; i < block; i += G) acc[i] = accumulate ? values[vbase + i] : 0.0;
+                    __syncwarp(gmask);
+                }
+                const int64_t rel = t - t0;
+                if ((rel & (kBlk - 1)) == 0 && rel > 0) {  // staging block boundary
+                    const int64_t blk = rel / kBlk;
+                    store_block(blk + 1);  // into the slot of block blk-1 (finished)
+                    load_block(blk + 2);
+                    __syncwarp(gmask);
+                }
+                const PosT* pk = pos_ring_t + (rel & (2 * kBlk - 1)) * pstride;
+                int q[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const uint32_t tb = tab[r];
+                    q[r] = static_cast<int>(tb & 1023u) * rowlen +
+                           static_cast<int>(pk[(tb >> 10) & 1023u]) * d + static_cast<int>(tb >> 20);
+                }
+                if (DISTINCT) {  // slots of one chunk are distinct: loads, adds, then stores
+                    double a[R];
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (r * G + gl < dm) a[r] = acc[q[r]];
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (r * G + gl < dm) acc[q[r]] = a[r] + kv[p][r];
+                } else {
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (r * G + gl < dm) acc[q[r]] += kv[p][r];
+                }
+                __syncwarp(gmask);
+                issue(p, t + PF);
+            }
+        }
+    }
+    for (;;) {  // the last node and any trailing empty nodes of the range
+        for (int i = gl; i < block; i += G) __stcs(values + vbase + i, acc[i]);
+        if (++v >= vend) break;
+        c0 = nptr[v];
+        rowlen = static_cast<int>(d * (nptr[v + 1] - c0));
+        block = d * rowlen;
+        vbase = static_cast<int64_t>(d) * d * c0;
+        __syncwarp(gmask);
+        for (int i = gl; i < block; i += G) acc[i] = accumulate ? values[vbase + i] : 0.0;
+        __syncwarp(gmask);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -311,7 +506,7 @@ __global__ void __launch_bounds__(kWarps * 32)
 // ---------------------------------------------------------------------------
 template <class PosT>
 __global__ void k_pos_elem(const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
-                           int64_t n_adj, int npe, const int32_t* __restrict__ k2l,
+                           int64_t n_adj, int npe, int pstride, const int32_t* __restrict__ k2l,
                            PosT* __restrict__ posE) {
     const int64_t total = n_adj * npe;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -322,7 +517,7 @@ __global__ void k_pos_elem(const int32_t* __restrict__ adj, const PosT* __restri
         const int32_t kr = entry / npe;
         const int a = entry - kr * npe;
         const int64_t le = k2l ? k2l[kr] : kr;
-        posE[(le * npe + a) * npe + b] = posA[t];
+        posE[(le * npe + a) * npe + b] = posA[k * pstride + b];
     }
 }
 
@@ -398,7 +593,37 @@ void cub_call(F&& f) {
 // --- launch helpers --------------------------------------------------------
 
 template <int G, int R, int PF, class PosT>
-void run_gather(fea_plan* p, const double* K, double* values, bool accumulate, cudaStream_t s) {
+void run_gather_stream(fea_plan* p, const double* K, double* values, bool accumulate, cudaStream_t s) {
+    constexpr int GPW = 32 / G;
+    const int acc_stride = p->d * p->d * p->max_cnt + 1;  // +1 staggers groups across banks
+    constexpr int kBlk = blk_of<G>();
+    const int pw_blk = kBlk * p->pstride * static_cast<int>(sizeof(PosT)) / 4;
+    FEA_REQUIRE((pw_blk + G - 1) / G <= kPosW, FEA_ERR_INVALID,
+                "position map of one element too large for the gather kernel's staging");
+    const size_t smem = static_cast<size_t>(kWarps) * GPW *
+                        (acc_stride * sizeof(double) + 2 * (kBlk + pw_blk) * sizeof(int32_t));
+    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID,
+                "node row block too large for shared-memory accumulation");
+    auto kern = p->dup_nodes ? k_gather_stream<G, R, PF, PosT, false> : k_gather_stream<G, R, PF, PosT, true>;
+    FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0, n_sm = 0;
+    FEA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kWarps * 32, smem));
+    FEA_CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, p->device));
+    if (p->n_own == 0) return;
+    // persistent: one wave of CTAs, each group a contiguous node range (>= 2 nodes per group)
+    int64_t blocks = static_cast<int64_t>(std::max(occ, 1)) * n_sm;
+    blocks = std::min<int64_t>(blocks, (p->n_own + 2 * kWarps * GPW - 1) / (2 * kWarps * GPW));
+    blocks = std::max<int64_t>(blocks, 1);
+    const int64_t n_groups = blocks * kWarps * GPW;
+    kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
+        K, p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->posA.as<PosT>(), p->nptr.as<int64_t>(),
+        p->n_own, n_groups, p->d, p->npe, p->pstride, acc_stride, accumulate ? 1 : 0, values);
+    FEA_CK(cudaGetLastError());
+    p->last_launches += 1;
+}
+
+template <int G, int R, int PF, class PosT>
+void run_gather_node(fea_plan* p, const double* K, double* values, bool accumulate, cudaStream_t s) {
     constexpr int GPW = 32 / G;
     const int acc_stride = p->d * p->d * p->max_cnt + 1;  // +1 staggers groups across banks
     const int pos_stride = static_cast<int>((std::max<int64_t>(p->max_adj, 1) * p->npe + 7) & ~int64_t(7));
@@ -406,7 +631,7 @@ void run_gather(fea_plan* p, const double* K, double* values, bool accumulate, c
                   (acc_stride * sizeof(double) + pos_stride * sizeof(PosT));
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID,
                 "node row block too large for shared-memory accumulation");
-    auto kern = p->dup_nodes ? k_gather<G, R, PF, PosT, false> : k_gather<G, R, PF, PosT, true>;
+    auto kern = p->dup_nodes ? k_gather_node<G, R, PF, PosT, false> : k_gather_node<G, R, PF, PosT, true>;
     if (smem > 48 * 1024)
         FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t groups = p->n_own;
@@ -414,10 +639,18 @@ void run_gather(fea_plan* p, const double* K, double* values, bool accumulate, c
     if (blocks == 0) return;
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
         K, p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->posA.as<PosT>(),
-        p->nptr.as<int64_t>(), p->n_own, p->d, p->npe, acc_stride, pos_stride,
+        p->nptr.as<int64_t>(), p->n_own, p->d, p->npe, p->pstride, acc_stride, pos_stride,
         accumulate ? 1 : 0, values);
     FEA_CK(cudaGetLastError());
     p->last_launches += 1;
+}
+
+// Kernel choice (measured): one lane group per warp (G == 32, large element
+// blocks) streams persistently; smaller blocks run one node per lane group, many warps.
+template <int G, int R, int PF, class PosT>
+void run_gather(fea_plan* p, const double* K, double* values, bool accumulate, cudaStream_t s) {
+    if (G == 32 && R >= 8) run_gather_stream<G, R, PF, PosT>(p, K, values, accumulate, s);
+    else run_gather_node<G, R, PF, PosT>(p, K, values, accumulate, s);
 }
 
 template <class PosT>
@@ -483,11 +716,11 @@ void ensure_element_maps(fea_plan* p, cudaStream_t s) {
     if (p->n_adj > 0) {
         if (p->pos_bytes == 1)
             k_pos_elem<uint8_t><<<grid_for(p->n_adj * p->npe, 256), 256, 0, s>>>(
-                p->adj.as<int32_t>(), p->posA.as<uint8_t>(), p->n_adj, p->npe, k2l_ptr,
+                p->adj.as<int32_t>(), p->posA.as<uint8_t>(), p->n_adj, p->npe, p->pstride, k2l_ptr,
                 p->posE.as<uint8_t>());
         else
             k_pos_elem<uint16_t><<<grid_for(p->n_adj * p->npe, 256), 256, 0, s>>>(
-                p->adj.as<int32_t>(), p->posA.as<uint16_t>(), p->n_adj, p->npe, k2l_ptr,
+                p->adj.as<int32_t>(), p->posA.as<uint16_t>(), p->n_adj, p->npe, p->pstride, k2l_ptr,
                 p->posE.as<uint16_t>());
     }
     FEA_CK(cudaGetLastError());

@@ -334,7 +334,7 @@ template <class PosT>
 __global__ void k_pos_adj(const int64_t* __restrict__ adj_ptr, const int32_t* __restrict__ adj,
                           const int32_t* __restrict__ conn_k, int npe, int64_t n_own,
                           const int64_t* __restrict__ nptr, const int32_t* __restrict__ ncol,
-                          PosT* __restrict__ posA) {
+                          int pstride, PosT* __restrict__ posA) {
     const int lane = threadIdx.x & 31;
     for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n_own;
          v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -344,7 +344,8 @@ __global__ void k_pos_adj(const int64_t* __restrict__ adj_ptr, const int32_t* __
         const int64_t cnt = nptr[v + 1] - nptr[v];
         for (int64_t i = lane; i < nc; i += 32) {
             const int32_t u = candidate(adj, conn_k, b0, npe, i);
-            posA[b0 * npe + i] = static_cast<PosT>(lower_bound_i32(list, cnt, u));
+            const int64_t k = i / npe;
+            posA[(b0 + k) * pstride + (i - k * npe)] = static_cast<PosT>(lower_bound_i32(list, cnt, u));
         }
     }
 }
@@ -444,8 +445,8 @@ __global__ void k_pos_external(const int64_t* __restrict__ adj_ptr, const int32_
                                const int32_t* __restrict__ conn_k, int npe, int64_t n_rows,
                                const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ cols,
                                const int64_t* __restrict__ crac_ptr,
-                               const int64_t* __restrict__ col_align, PosT* __restrict__ posA,
-                               unsigned long long* __restrict__ miss) {
+                               const int64_t* __restrict__ col_align, int pstride,
+                               PosT* __restrict__ posA, unsigned long long* __restrict__ miss) {
     const int lane = threadIdx.x & 31;
     for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n_rows;
          r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -480,7 +481,7 @@ __global__ void k_pos_external(const int64_t* __restrict__ adj_ptr, const int32_
                 atomicMin(miss, static_cast<unsigned long long>((e * npe + a) * npe + b));
                 pos = lo0;
             }
-            posA[b0 * npe + i] = static_cast<PosT>(pos - lo0);
+            posA[(b0 + i / npe) * pstride + i % npe] = static_cast<PosT>(pos - lo0);
         }
     }
 }
@@ -586,6 +587,7 @@ void finish_counts(fea_plan* p, DevBuf& counts, cudaStream_t s) {
                 "a pattern row has more than 65536 column nodes (position map limit)");
     p->max_cnt = static_cast<int32_t>(h);
     p->pos_bytes = h <= 256 ? 1 : 2;
+    p->pstride = ((p->npe * p->pos_bytes + 3) / 4 * 4) / p->pos_bytes;
     p->nnz = static_cast<int64_t>(p->d) * p->d * p->nnz_nodes;
 }
 
@@ -658,16 +660,17 @@ void build_own_pattern(fea_plan* p, cudaStream_t s) {
             big.as<int32_t>(), nullptr, p->nptr.as<int64_t>(), p->ncol.as<int32_t>());
     FEA_CK(cudaGetLastError());
     // slot map (adjacency order)
-    p->posA.alloc(p->n_adj * p->npe * p->pos_bytes + 64);  // slack: 16B-rounded bulk copies
+    p->posA.alloc(p->n_adj * p->pstride * p->pos_bytes + 64);
+    FEA_CK(cudaMemsetAsync(p->posA.p, 0, p->posA.bytes, s));
     if (p->n_own > 0) {
         if (p->pos_bytes == 1)
             k_pos_adj<uint8_t><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
                 p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
-                p->n_own, p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->posA.as<uint8_t>());
+                p->n_own, p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->pstride, p->posA.as<uint8_t>());
         else
             k_pos_adj<uint16_t><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
                 p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
-                p->n_own, p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->posA.as<uint16_t>());
+                p->n_own, p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->pstride, p->posA.as<uint16_t>());
         FEA_CK(cudaGetLastError());
     }
     build_runs(p, s);
@@ -840,7 +843,6 @@ fea_status fea_plan_create(int device, const int64_t* elem_dofs, int64_t n_eleme
         Stream st;
         auto p = std::make_unique<fea_plan>();
         p->device = device;
-        p->tma_disabled = std::getenv("FEA_GATHER_NO_TMA") != nullptr;
         p->E_in = n_elements;
         p->m = m;
         p->n_rows = n_rows;
@@ -931,6 +933,7 @@ fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, in
         FEA_REQUIRE(max_len <= 65536, FEA_ERR_INVALID, "pattern row longer than 65536 entries");
         p->max_cnt = static_cast<int32_t>(max_len);
         p->pos_bytes = max_len <= 256 ? 1 : 2;
+        p->pstride = ((p->npe * p->pos_bytes + 3) / 4 * 4) / p->pos_bytes;
         p->nnz_nodes = nnz;
         p->nnz = nnz;
         // device copies for the lookup kernel
@@ -950,14 +953,15 @@ fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, in
         }
         miss.alloc(8);
         FEA_CK(cudaMemsetAsync(miss.p, 0xff, 8, s));
-        p->posA.alloc(p->n_adj * p->npe * p->pos_bytes + 64);
+        p->posA.alloc(p->n_adj * p->pstride * p->pos_bytes + 64);
+        FEA_CK(cudaMemsetAsync(p->posA.p, 0, p->posA.bytes, s));
         const unsigned blocks = grid_for(n_rows * 32, 256);
         if (n_rows > 0) {
 #define FEA_LAUNCH_EXT(T, C)                                                                   \
     k_pos_external<T, C><<<blocks, 256, 0, s>>>(                                               \
         p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe, n_rows, \
         d_ptr.as<int64_t>(), d_cols.as<int64_t>(), d_cptr.as<int64_t>(), d_align.as<int64_t>(), \
-        p->posA.as<T>(), miss.as<unsigned long long>())
+        p->pstride, p->posA.as<T>(), miss.as<unsigned long long>())
             const bool crac = format == FEA_FORMAT_CRAC;
             if (p->pos_bytes == 1) {
                 if (crac) FEA_LAUNCH_EXT(uint8_t, true); else FEA_LAUNCH_EXT(uint8_t, false);
