@@ -147,13 +147,14 @@ FEA_API fea_status fea_plan_copy_elements(const fea_plan* plan, int64_t* elem_id
 
 /* Greedy colouring of the plan's elements — fea::greedy_colouring
  * (colouring.cpp:24-75): ascending element order, smallest colour unused by any
- * node-sharing element. colour_of[E] (host). */
+ * node-sharing element. colour_of[n_elements] (host; the plan's kept elements in
+ * ascending id, = all E for a whole-matrix plan). */
 FEA_API fea_status fea_plan_greedy_colouring(const fea_plan* plan, int32_t* colour_of, int32_t* n_colours);
 
 /* Install the colouring used by FEA_DET_COLOUR (Colouring::colour_of,
- * colouring.hpp:35-39; host array over all E input elements). Validated like
- * find_colour_conflict (colouring.cpp:91-119): two same-colour elements sharing
- * a DOF -> FEA_ERR_INVALID_COLOURING. */
+ * colouring.hpp:35-39; host or device array over the plan's kept elements).
+ * Validated like find_colour_conflict (colouring.cpp:91-119): two same-colour
+ * elements sharing a DOF -> FEA_ERR_INVALID_COLOURING. */
 FEA_API fea_status fea_plan_set_colouring(fea_plan* plan, const int32_t* colour_of);
 
 /*
