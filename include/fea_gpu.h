@@ -176,6 +176,16 @@ FEA_API fea_status fea_assemble(fea_plan* plan, const double* K, int32_t strateg
 FEA_API fea_status fea_assemble_host(fea_plan* plan, const double* K_host, int32_t strategy,
                              double* values_host, uint32_t flags, void* stream);
 
+/* Repeated end-to-end assemblies of the same plan with new element matrices (Newton
+ * iterations, time steps, load cases): n_steps pairs of HOST buffers K_hosts[i] ->
+ * values_hosts[i]. Pipelined with two device staging slots: step i's K host->device copy
+ * overlaps step i-1's kernel and values device->host copy (PCIe is full duplex). Every step
+ * moves its whole K in and its whole values out; synchronous on return. Pinned host memory
+ * is required for the overlap. */
+FEA_API fea_status fea_assemble_host_batch(fea_plan* plan, const double* const* K_hosts,
+                                           int32_t strategy, double* const* values_hosts,
+                                           int32_t n_steps, uint32_t flags, void* stream);
+
 /* The missing entry behind FEA_ERR_MISSING_ENTRY: element, row, column (the
  * values AssemblyError names, assembly.hpp:65-73). Returns FEA_OK with e = -1
  * when the plan has none. */

@@ -181,6 +181,19 @@ class Plan:
                                            _ptr(values_host), flags, _stream_ptr(stream)))
         return values_host
 
+    def assemble_host_batch(self, K_hosts, values_hosts, strategy: str = "sorted",
+                            accumulate: bool = False, stream=None):
+        """Pipelined repeated end-to-end assemblies: K_hosts[i] (host) -> values_hosts[i] (host).
+        Step i's K upload overlaps step i-1's kernel and values download (pinned memory)."""
+        n = len(K_hosts)
+        assert len(values_hosts) == n
+        kp = (c_void_p * max(n, 1))(*[_ptr(k).value for k in K_hosts])
+        vp = (c_void_p * max(n, 1))(*[_ptr(v).value for v in values_hosts])
+        flags = N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE
+        _check(self._lib.fea_assemble_host_batch(self._h, kp, STRATEGIES[strategy], vp, n, flags,
+                                                 _stream_ptr(stream)))
+        return values_hosts
+
     def close(self) -> None:
         if self._h and self._h.value:
             self._lib.fea_plan_destroy(self._h)

@@ -107,6 +107,7 @@ struct fea_plan {
     // bookkeeping
     int32_t last_launches = 0;
     feagpu::DevBuf stage_K, stage_V;       // fea_assemble_host staging
+    feagpu::DevBuf bstage_K[2], bstage_V[2];  // fea_assemble_host_batch double buffers
     int64_t kbytes_required() const;
     int64_t krows() const { return k_compact ? E : E_in; }
 };

@@ -660,7 +660,10 @@ void gather(fea_plan* p, const double* K, double* values, bool accumulate, cudaS
     else if (dm <= 8) run_gather<8, 1, 8, PosT>(p, K, values, accumulate, s);
     else if (dm <= 16) run_gather<16, 1, 4, PosT>(p, K, values, accumulate, s);
     else if (dm <= 32) run_gather<32, 1, 4, PosT>(p, K, values, accumulate, s);
-    else if (dm == 72) run_gather<8, 9, 2, PosT>(p, K, values, accumulate, s);
+#ifndef FEA_HEX8_PF
+#define FEA_HEX8_PF 2
+#endif
+    else if (dm == 72) run_gather<8, 9, FEA_HEX8_PF, PosT>(p, K, values, accumulate, s);
     else if (dm <= 128) run_gather<32, 4, 2, PosT>(p, K, values, accumulate, s);
     else if (dm <= 256) run_gather<32, 8, 2, PosT>(p, K, values, accumulate, s);
     else if (dm <= 512) run_gather<32, 16, 1, PosT>(p, K, values, accumulate, s);
@@ -846,6 +849,78 @@ fea_status fea_assemble_host(fea_plan* plan, const double* K_host, int32_t strat
         assemble(plan, plan->stage_K.as<double>(), strategy, plan->stage_V.as<double>(), flags, s);
         if (vb) FEA_CK(cudaMemcpyAsync(values_host, plan->stage_V.p, vb, cudaMemcpyDeviceToHost, s));
         FEA_CK(cudaStreamSynchronize(s));
+    });
+}
+
+// Repeated end-to-end assemblies (new element matrices each step, e.g. Newton or time
+// steps): step i's K host->device copy overlaps step i-1's values device->host copy and
+// kernel (full-duplex PCIe, separate copy streams), with two device staging slots.
+// Every step still moves its whole K in and its whole values array out. Synchronous.
+fea_status fea_assemble_host_batch(fea_plan* plan, const double* const* K_hosts, int32_t strategy,
+                                   double* const* values_hosts, int32_t n_steps, uint32_t flags,
+                                   void* stream) {
+    return guarded_n([&] {
+        FEA_REQUIRE(plan && n_steps >= 0 && (n_steps == 0 || (K_hosts && values_hosts)),
+                    FEA_ERR_INVALID, "bad arguments");
+        DeviceScope ds(plan->device);
+        cudaStream_t sc = static_cast<cudaStream_t>(stream);
+        const size_t kb = static_cast<size_t>(plan->kbytes_required());
+        const size_t vb = static_cast<size_t>(plan->nnz) * 8;
+        for (int s2 = 0; s2 < 2; ++s2) {
+            if (plan->bstage_K[s2].bytes < kb) plan->bstage_K[s2].alloc(kb);
+            if (plan->bstage_V[s2].bytes < vb) plan->bstage_V[s2].alloc(vb);
+        }
+        cudaStream_t sin = nullptr, sout = nullptr;
+        FEA_CK(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
+        FEA_CK(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
+        cudaEvent_t ev_in[2], ev_done[2], ev_out[2];
+        for (int s2 = 0; s2 < 2; ++s2) {
+            FEA_CK(cudaEventCreateWithFlags(&ev_in[s2], cudaEventDisableTiming));
+            FEA_CK(cudaEventCreateWithFlags(&ev_done[s2], cudaEventDisableTiming));
+            FEA_CK(cudaEventCreateWithFlags(&ev_out[s2], cudaEventDisableTiming));
+        }
+        int32_t launches = 0;
+        try {
+            for (int32_t i = 0; i < n_steps; ++i) {
+                const int sl = i & 1;
+                double* dK = plan->bstage_K[sl].as<double>();
+                double* dV = plan->bstage_V[sl].as<double>();
+                if (i >= 2) {  // slot reuse: kernel i-2 done with K, copy-out i-2 done with values
+                    FEA_CK(cudaStreamWaitEvent(sin, ev_done[sl], 0));
+                    FEA_CK(cudaStreamWaitEvent(sin, ev_out[sl], 0));
+                }
+                if (kb) FEA_CK(cudaMemcpyAsync(dK, K_hosts[i], kb, cudaMemcpyHostToDevice, sin));
+                if (!(flags & FEA_OVERWRITE) && vb)
+                    FEA_CK(cudaMemcpyAsync(dV, values_hosts[i], vb, cudaMemcpyHostToDevice, sin));
+                FEA_CK(cudaEventRecord(ev_in[sl], sin));
+                FEA_CK(cudaStreamWaitEvent(sc, ev_in[sl], 0));
+                assemble(plan, dK, strategy, dV, flags, sc);
+                launches += plan->last_launches;
+                FEA_CK(cudaEventRecord(ev_done[sl], sc));
+                FEA_CK(cudaStreamWaitEvent(sout, ev_done[sl], 0));
+                if (vb) FEA_CK(cudaMemcpyAsync(values_hosts[i], dV, vb, cudaMemcpyDeviceToHost, sout));
+                FEA_CK(cudaEventRecord(ev_out[sl], sout));
+            }
+            FEA_CK(cudaStreamSynchronize(sin));
+            FEA_CK(cudaStreamSynchronize(sc));
+            FEA_CK(cudaStreamSynchronize(sout));
+        } catch (...) {
+            cudaStreamSynchronize(sin);
+            cudaStreamSynchronize(sc);
+            cudaStreamSynchronize(sout);
+            for (int s2 = 0; s2 < 2; ++s2) {
+                cudaEventDestroy(ev_in[s2]); cudaEventDestroy(ev_done[s2]); cudaEventDestroy(ev_out[s2]);
+            }
+            cudaStreamDestroy(sin);
+            cudaStreamDestroy(sout);
+            throw;
+        }
+        for (int s2 = 0; s2 < 2; ++s2) {
+            cudaEventDestroy(ev_in[s2]); cudaEventDestroy(ev_done[s2]); cudaEventDestroy(ev_out[s2]);
+        }
+        cudaStreamDestroy(sin);
+        cudaStreamDestroy(sout);
+        plan->last_launches = launches;
     });
 }
 

@@ -271,3 +271,26 @@ def test_gpu_matches_reference_fixtures(gpu, orc, name):
         ones = torch.ones((E, m, m), dtype=torch.float64, device="cuda")
         for s in ("sorted", "atomic", "colour"):
             assert plan.assemble(ones, strategy=s).cpu().numpy().tobytes() == g["values_ones"].tobytes()
+
+
+def test_host_batch_pipeline(gpu, orc):
+    """fea_assemble_host_batch: several steps with different K, each bit-exact vs sequential."""
+    import torch
+    conn, nn, ed, n_rows = problem("hex8", 3, 3, "elements")
+    P = orc.Pattern.build(conn, nn, 3)
+    Ks = [orc.fill_k(s, conn.shape[0], ed.shape[1]) for s in (1, 2, 3, 4, 5)]
+    vals = [np.zeros(P.nnz) for _ in Ks]
+    with gpu.Plan(ed, n_rows, dofs_per_node=3) as plan:
+        for strategy in ("sorted", "atomic"):
+            plan.assemble_host_batch(Ks, vals, strategy=strategy)
+            for K, v in zip(Ks, vals):
+                want = P.assemble_sequential(ed, K)
+                if strategy == "sorted":
+                    assert v.tobytes() == want.tobytes()
+                else:
+                    assert close(v, want)
+        # accumulate: values are uploaded, added to, downloaded
+        start = [np.full(P.nnz, 0.5) for _ in Ks[:2]]
+        plan.assemble_host_batch(Ks[:2], start, strategy="sorted", accumulate=True)
+        for K, v in zip(Ks[:2], start):
+            assert v.tobytes() == P.assemble_sequential(ed, K, np.full(P.nnz, 0.5)).tobytes()
