@@ -53,6 +53,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gather", action="store_true", help="NCCL gather of row blocks to rank 0 (N>1)")
+    ap.add_argument("--check", action="store_true",
+                    help="with --gather: rank 0 re-assembles the global mesh on its GPU and compares bitwise")
     return ap.parse_args()
 
 
@@ -186,10 +188,17 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     N = world
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; FEA_BENCH_BACKEND=gloo lets N ranks share fewer GPUs for a
+    # functional check of this path (timings from such a run are not scaling numbers)
+    backend = os.environ.get("FEA_BENCH_BACKEND", "nccl")
+    dev = torch.device("cuda", local % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    red_dev = dev if backend == "nccl" else torch.device("cpu")
 
     conn, n_nodes = global_mesh(N)
     E_glob = conn.shape[0]
@@ -198,12 +207,12 @@ def run_ours(args):
     n_rows = n_nodes * D
     rb, re = owned_rows(N, rank)
     t0 = time.perf_counter()
-    plan = fea.Plan(ed, n_rows, dofs_per_node=D, row_range=(rb, re), device=local, k_compact=N > 1)
+    plan = fea.Plan(ed, n_rows, dofs_per_node=D, row_range=(rb, re), device=dev.index, k_compact=N > 1)
     torch.cuda.synchronize()
     symbolic_ms = (time.perf_counter() - t0) * 1e3
     E_loc = plan.n_elements
     ids = plan.elements() if N > 1 else None
-    K = fea.fill_seeded_k(E_loc, m, SEED_K, elem_ids=ids, device=local)
+    K = fea.fill_seeded_k(E_loc, m, SEED_K, elem_ids=ids, device=dev.index)
     values = torch.zeros(plan.nnz, dtype=torch.float64, device=dev)
     colour, n_colours = plan.greedy_colouring()
     plan.set_colouring(colour)
@@ -253,13 +262,13 @@ def run_ours(args):
             continue
         tot, ms, _ = timed(s, max(3, args.steps // 2), args.warmup)
         results[s] = tot / len(ms)
-    with ClockSampler(local) as cs:
+    with ClockSampler(dev.index) as cs:
         total_ms, ms_list, launches = timed(args.strategy, args.steps, args.warmup, sampler=cs)
     clocks = cs.summary()
     results[args.strategy] = total_ms / args.steps
 
     # max over ranks (device time)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_max = float(t.item())
@@ -302,7 +311,7 @@ def run_ours(args):
         for i in range(3):
             plan.assemble_host(Kh_np[0], vh_np[0], strategy=args.strategy, stream=stream)
         single_s = (time.perf_counter() - t1) / 3
-        te = torch.tensor([e2e_s, single_s], dtype=torch.float64, device=dev)
+        te = torch.tensor([e2e_s, single_s], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": entries / float(te[0].item()), "unit": UNIT,
@@ -318,13 +327,24 @@ def run_ours(args):
         del Kh, vh, Kh_np, vh_np, ks, vs
 
     gather_ms = None
+    gathered_nnz = None
+    check_ok = None
     if args.gather and world > 1:
         from paper_2012_00585_b200.dist import gather_row_blocks
         torch.cuda.synchronize()
+        dist.barrier()
         tg = time.perf_counter()
-        gather_row_blocks(values, root=0)
+        full = gather_row_blocks(values if backend == "nccl" else values.cpu(), root=0)
         torch.cuda.synchronize()
         gather_ms = (time.perf_counter() - tg) * 1e3
+        if rank == 0:
+            gathered_nnz = int(full.numel())
+            if args.check:
+                gplan = fea.Plan(ed, n_rows, dofs_per_node=D, device=dev.index)
+                gK = fea.fill_seeded_k(E_glob, m, SEED_K, device=dev.index)
+                want = gplan.assemble(gK, strategy=args.strategy if args.strategy == "sorted" else "sorted")
+                check_ok = bool(torch.equal(full.to(dev), want)) if args.strategy == "sorted" else None
+                del gplan, gK, want
 
     cpu_baseline = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
@@ -353,7 +373,10 @@ def run_ours(args):
             "cpu_baseline": cpu_baseline,
         }
         if gather_ms is not None:
-            line["nccl_gather_ms"] = gather_ms
+            line["gather"] = {"ms": gather_ms, "backend": backend, "rows_blocks_nnz_total": gathered_nnz,
+                              "bitwise_equal_to_single_gpu": check_ok}
+        if backend != "nccl":
+            line["note"] = f"functional run over {backend} with {world} ranks on {torch.cuda.device_count()} GPU(s): not a scaling measurement"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -431,8 +454,17 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _relaunch_under_torchrun(n: int) -> int:
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", os.environ.get("MASTER_PORT", "29533"),
+           __file__, *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 if __name__ == "__main__":
     a = parse_args()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch_under_torchrun(a.gpus))
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -1,0 +1,57 @@
+"""bench.py keeps the driver's JSON contract (both arms)."""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+             "scaling", "vs_baseline", "dtype", "data", "config"}
+
+
+def run(args, env=None, timeout=900):
+    e = dict(os.environ)
+    e.update(env or {})
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], capture_output=True, text=True,
+                       timeout=timeout, env=e, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+@pytest.mark.timeout(600)
+def test_reference_arm_contract(ref_lib):
+    """--impl reference: the reference library on the host cores, same workload and metric."""
+    d = run(["--impl", "reference", "--steps", "2", "--warmup", "1"])
+    assert BASE_KEYS <= set(d)
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "entries/s"
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(900)
+def test_gpu_arm_contract(gpu):
+    d = run(["--steps", "3", "--warmup", "3", "--no-cpu-baseline"])
+    assert BASE_KEYS <= set(d)
+    assert d["n_gpus"] == 1 and d["dtype"] == "f64" and d["higher_is_better"] is True
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and 0 < r["frac"] < 1.2 and r["unit"] == "GB/s"
+    assert d["gpu_launches"] == 3
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["clocks"]["sm_mhz"] is not None
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(900)
+def test_two_rank_partitioned_bench_matches_single_gpu(gpu):
+    """torchrun, 2 ranks over gloo sharing the box's GPU: the row-partitioned path end to end;
+    the gathered row blocks equal a single-GPU assembly of the global mesh bit for bit."""
+    d = run(["--gpus", "2", "--steps", "2", "--warmup", "3", "--gather", "--check", "--no-e2e"],
+            env={"FEA_BENCH_BACKEND": "gloo", "MASTER_PORT": "29541"})
+    assert d["n_gpus"] == 2 and d["gather"]["bitwise_equal_to_single_gpu"] is True
