@@ -49,7 +49,7 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--strategy", default="sorted", choices=["sorted", "atomic", "colour"])
+    ap.add_argument("--strategy", default="sorted", choices=["sorted", "atomic", "colour", "colour_passes"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gather", action="store_true", help="NCCL gather of row blocks to rank 0 (N>1)")
@@ -226,7 +226,8 @@ def run_ours(args):
 
     def timed(strategy, steps, warmup, sampler=None):
         """Per step: untimed reset (atomic/colour) + L2 flush, then events around the assembly."""
-        acc = strategy != "sorted"  # sorted overwrites (== reset + assemble); others add into zeros
+        acc = strategy in ("atomic", "colour_passes")  # element-owner routes add into a reset values array;
+        # the segmented reductions overwrite (== reset_values + assemble, same bits)
         for _ in range(warmup):
             if acc:
                 values.zero_()
@@ -257,7 +258,7 @@ def run_ours(args):
         return sum(ms), ms, launches
 
     results = {}
-    for s in ("sorted", "atomic", "colour"):
+    for s in ("sorted", "atomic", "colour", "colour_passes"):
         if s == args.strategy:
             continue
         tot, ms, _ = timed(s, max(3, args.steps // 2), args.warmup)
@@ -283,7 +284,8 @@ def run_ours(args):
     peak, peak_src = measured_peak_gbs()
     achieved = min_bytes / (my_ms * 1e-3) / 1e9
     kernel_name = {"sorted": "k_gather<8,9,2,u8>", "atomic": "k_scatter<32,u8,atomic>",
-                   "colour": "k_scatter<32,u8,plain> x n_colours"}[args.strategy]
+                   "colour": "k_gather_node<8,9,2,u8> (colour-ordered incidences)",
+                   "colour_passes": "k_scatter<32,u8,plain> x n_colours"}[args.strategy]
     traffic = profiled_traffic(f"cfg2/{args.strategy}") if N == 1 else None
 
     # end to end through the public API with HOST buffers (pinned): every step copies its whole

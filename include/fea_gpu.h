@@ -70,6 +70,8 @@ typedef enum {
 /* fea_assemble flags */
 #define FEA_ACCUMULATE 0u /* values += assembled (reference semantics: assemble adds) */
 #define FEA_OVERWRITE 1u  /* values  = assembled (== reset_values, formats.hpp:351-354, then assemble) */
+#define FEA_COLOUR_PASSES 2u /* FEA_DET_COLOUR as one launch per colour (element-owner, plain adds)
+                              instead of the colour-ordered segmented reduction; same bits */
 
 /* fea_plan_create flags */
 #define FEA_PLAN_K_COMPACT 1u /* K holds only the plan's kept elements, in ascending element id

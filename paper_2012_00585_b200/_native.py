@@ -26,6 +26,7 @@ FEA_DET_COLOUR = 2
 
 FEA_ACCUMULATE = 0
 FEA_OVERWRITE = 1
+FEA_COLOUR_PASSES = 2
 FEA_PLAN_K_COMPACT = 1
 FEA_FORMAT_CSR = 0
 FEA_FORMAT_CRAC = 1

@@ -19,7 +19,11 @@ import numpy as np
 
 from . import _native as N
 
-STRATEGIES = {"atomic": N.FEA_ATOMIC, "sorted": N.FEA_DET_SORTED, "colour": N.FEA_DET_COLOUR}
+STRATEGIES = {"atomic": N.FEA_ATOMIC, "sorted": N.FEA_DET_SORTED, "colour": N.FEA_DET_COLOUR,
+              "colour_passes": N.FEA_DET_COLOUR}
+# "colour": colour-ordered segmented reduction; "colour_passes": one launch per colour
+# (element owner, plain adds). Both are bit-identical to assemble_coloured_vectorized.
+_EXTRA_FLAGS = {"colour_passes": N.FEA_COLOUR_PASSES}
 
 
 class FeaError(RuntimeError):
@@ -165,7 +169,7 @@ class Plan:
         if values is None:
             values = torch.zeros(self.nnz, dtype=torch.float64, device=f"cuda:{self.device}")
             accumulate = False
-        flags = N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE
+        flags = (N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE) | _EXTRA_FLAGS.get(strategy, 0)
         _check(self._lib.fea_assemble(self._h, _ptr(K), STRATEGIES[strategy], _ptr(values), flags,
                                       _stream_ptr(stream)))
         return values
@@ -176,7 +180,7 @@ class Plan:
         if values_host is None:
             values_host = np.zeros(self.nnz, np.float64)
             accumulate = False
-        flags = N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE
+        flags = (N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE) | _EXTRA_FLAGS.get(strategy, 0)
         _check(self._lib.fea_assemble_host(self._h, _ptr(K_host), STRATEGIES[strategy],
                                            _ptr(values_host), flags, _stream_ptr(stream)))
         return values_host
@@ -189,7 +193,7 @@ class Plan:
         assert len(values_hosts) == n
         kp = (c_void_p * max(n, 1))(*[_ptr(k).value for k in K_hosts])
         vp = (c_void_p * max(n, 1))(*[_ptr(v).value for v in values_hosts])
-        flags = N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE
+        flags = (N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE) | _EXTRA_FLAGS.get(strategy, 0)
         _check(self._lib.fea_assemble_host_batch(self._h, kp, STRATEGIES[strategy], vp, n, flags,
                                                  _stream_ptr(stream)))
         return values_hosts

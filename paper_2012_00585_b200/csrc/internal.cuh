@@ -101,6 +101,7 @@ struct fea_plan {
     // colouring
     bool has_colouring = false;
     feagpu::DevBuf colour_elems;           // int32 [E] local elements grouped by colour, ascending id
+    feagpu::DevBuf adjC, posAC;            // incidences per node in (colour, element) order + positions
     std::vector<int64_t> colour_off;       // n_colours+1 (host)
     // external-pattern missing entry (lowest element)
     int64_t miss_e = -1, miss_r = -1, miss_c = -1;

@@ -29,6 +29,13 @@ namespace {
 
 constexpr int kWarps = 4;  // warps per CTA for the numeric kernels
 
+// Per-node incidence order used by the gather: ascending element id (FEA_DET_SORTED) or
+// ascending (colour, element id) (FEA_DET_COLOUR), with the matching position rows.
+struct Incidences {
+    const int32_t* adj;
+    const void* posA;
+};
+
 unsigned grid_for(int64_t n, int threads) {
     int64_t b = (n + threads - 1) / threads;
     if (b < 1) b = 1;
@@ -593,7 +600,8 @@ void cub_call(F&& f) {
 // --- launch helpers --------------------------------------------------------
 
 template <int G, int R, int PF, class PosT>
-void run_gather_stream(fea_plan* p, const double* K, double* values, bool accumulate, cudaStream_t s) {
+void run_gather_stream(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
+                       cudaStream_t s) {
     constexpr int GPW = 32 / G;
     const int acc_stride = p->d * p->d * p->max_cnt + 1;  // +1 staggers groups across banks
     constexpr int kBlk = blk_of<G>();
@@ -616,14 +624,15 @@ void run_gather_stream(fea_plan* p, const double* K, double* values, bool accumu
     blocks = std::max<int64_t>(blocks, 1);
     const int64_t n_groups = blocks * kWarps * GPW;
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
-        K, p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->posA.as<PosT>(), p->nptr.as<int64_t>(),
+        K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const PosT*>(in.posA), p->nptr.as<int64_t>(),
         p->n_own, n_groups, p->d, p->npe, p->pstride, acc_stride, accumulate ? 1 : 0, values);
     FEA_CK(cudaGetLastError());
     p->last_launches += 1;
 }
 
 template <int G, int R, int PF, class PosT>
-void run_gather_node(fea_plan* p, const double* K, double* values, bool accumulate, cudaStream_t s) {
+void run_gather_node(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
+                     cudaStream_t s) {
     constexpr int GPW = 32 / G;
     const int acc_stride = p->d * p->d * p->max_cnt + 1;  // +1 staggers groups across banks
     const int pos_stride = static_cast<int>((std::max<int64_t>(p->max_adj, 1) * p->npe + 7) & ~int64_t(7));
@@ -638,7 +647,7 @@ void run_gather_node(fea_plan* p, const double* K, double* values, bool accumula
     const int64_t blocks = (groups + kWarps * GPW - 1) / (kWarps * GPW);
     if (blocks == 0) return;
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
-        K, p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->posA.as<PosT>(),
+        K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const PosT*>(in.posA),
         p->nptr.as<int64_t>(), p->n_own, p->d, p->npe, p->pstride, acc_stride, pos_stride,
         accumulate ? 1 : 0, values);
     FEA_CK(cudaGetLastError());
@@ -648,25 +657,27 @@ void run_gather_node(fea_plan* p, const double* K, double* values, bool accumula
 // Kernel choice (measured): one lane group per warp (G == 32, large element
 // blocks) streams persistently; smaller blocks run one node per lane group, many warps.
 template <int G, int R, int PF, class PosT>
-void run_gather(fea_plan* p, const double* K, double* values, bool accumulate, cudaStream_t s) {
-    if (G == 32 && R >= 8) run_gather_stream<G, R, PF, PosT>(p, K, values, accumulate, s);
-    else run_gather_node<G, R, PF, PosT>(p, K, values, accumulate, s);
+void run_gather(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
+                cudaStream_t s) {
+    if (G == 32 && R >= 8) run_gather_stream<G, R, PF, PosT>(p, in, K, values, accumulate, s);
+    else run_gather_node<G, R, PF, PosT>(p, in, K, values, accumulate, s);
 }
 
 template <class PosT>
-void gather(fea_plan* p, const double* K, double* values, bool accumulate, cudaStream_t s) {
+void gather(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
+            cudaStream_t s) {
     const int dm = p->d * p->m;
-    if (dm <= 4) run_gather<4, 1, 8, PosT>(p, K, values, accumulate, s);
-    else if (dm <= 8) run_gather<8, 1, 8, PosT>(p, K, values, accumulate, s);
-    else if (dm <= 16) run_gather<16, 1, 4, PosT>(p, K, values, accumulate, s);
-    else if (dm <= 32) run_gather<32, 1, 4, PosT>(p, K, values, accumulate, s);
+    if (dm <= 4) run_gather<4, 1, 8, PosT>(p, in, K, values, accumulate, s);
+    else if (dm <= 8) run_gather<8, 1, 8, PosT>(p, in, K, values, accumulate, s);
+    else if (dm <= 16) run_gather<16, 1, 4, PosT>(p, in, K, values, accumulate, s);
+    else if (dm <= 32) run_gather<32, 1, 4, PosT>(p, in, K, values, accumulate, s);
 #ifndef FEA_HEX8_PF
 #define FEA_HEX8_PF 2
 #endif
-    else if (dm == 72) run_gather<8, 9, FEA_HEX8_PF, PosT>(p, K, values, accumulate, s);
-    else if (dm <= 128) run_gather<32, 4, 2, PosT>(p, K, values, accumulate, s);
-    else if (dm <= 256) run_gather<32, 8, 2, PosT>(p, K, values, accumulate, s);
-    else if (dm <= 512) run_gather<32, 16, 1, PosT>(p, K, values, accumulate, s);
+    else if (dm == 72) run_gather<8, 9, FEA_HEX8_PF, PosT>(p, in, K, values, accumulate, s);
+    else if (dm <= 128) run_gather<32, 4, 2, PosT>(p, in, K, values, accumulate, s);
+    else if (dm <= 256) run_gather<32, 8, 2, PosT>(p, in, K, values, accumulate, s);
+    else if (dm <= 512) run_gather<32, 16, 1, PosT>(p, in, K, values, accumulate, s);
     else throw Error(FEA_ERR_INVALID, "element row block (d*m) larger than 512 entries");
 }
 
@@ -777,14 +788,19 @@ void assemble(fea_plan* p, const double* K, int strategy, double* values, uint32
     FEA_REQUIRE(p->E == 0 || K, FEA_ERR_INVALID, "K is NULL");
     const bool overwrite = (flags & FEA_OVERWRITE) != 0;
     p->last_launches = 0;
-    if (strategy == FEA_DET_SORTED) {
-        if (p->pos_bytes == 1) gather<uint8_t>(p, K, values, !overwrite, s);
-        else gather<uint16_t>(p, K, values, !overwrite, s);
-        return;
-    }
     if (strategy == FEA_DET_COLOUR)
         FEA_REQUIRE(p->has_colouring, FEA_ERR_INVALID,
                     "FEA_DET_COLOUR needs a colouring (fea_plan_set_colouring)");
+    if (strategy == FEA_DET_SORTED || (strategy == FEA_DET_COLOUR && !(flags & FEA_COLOUR_PASSES))) {
+        // DET_COLOUR as a segmented reduction: within each node the incidences are ordered by
+        // (colour, element), so every slot folds its contributions in colour order — exactly
+        // the summation order of the per-colour passes of assemble_coloured_vectorized.
+        Incidences in{p->adj.as<int32_t>(), p->posA.p};
+        if (strategy == FEA_DET_COLOUR) in = Incidences{p->adjC.as<int32_t>(), p->posAC.p};
+        if (p->pos_bytes == 1) gather<uint8_t>(p, in, K, values, !overwrite, s);
+        else gather<uint16_t>(p, in, K, values, !overwrite, s);
+        return;
+    }
     ensure_element_maps(p, s);
     if (overwrite && p->nnz > 0) FEA_CK(cudaMemsetAsync(values, 0, p->nnz * 8, s));
     if (strategy == FEA_ATOMIC) {

@@ -486,6 +486,45 @@ __global__ void k_pos_external(const int64_t* __restrict__ adj_ptr, const int32_
     }
 }
 
+// Colour-ordered incidences (FEA_DET_COLOUR as a segmented reduction): keys for a
+// two-pass LSD stable sort, first by colour, then by node — each node's incidences end up
+// in ascending (colour, element id).
+__global__ void k_node_of(const int64_t* __restrict__ adj_ptr, int64_t n_own, int32_t* __restrict__ node_of) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n_own;
+         v += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t k = adj_ptr[v]; k < adj_ptr[v + 1]; ++k) node_of[k] = static_cast<int32_t>(v);
+}
+
+__global__ void k_colour_keys(const int32_t* __restrict__ adj, int64_t n_adj, int npe,
+                              const int32_t* __restrict__ colour_of_krow, uint32_t* __restrict__ keys,
+                              int32_t* __restrict__ vals) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_adj;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        keys[k] = static_cast<uint32_t>(colour_of_krow[adj[k] / npe]);
+        vals[k] = static_cast<int32_t>(k);
+    }
+}
+
+__global__ void k_gather_keys(const int32_t* __restrict__ node_of, const int32_t* __restrict__ perm,
+                              int64_t n, uint32_t* __restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        keys[i] = static_cast<uint32_t>(node_of[perm[i]]);
+}
+
+__global__ void k_permute_incidences(const int32_t* __restrict__ perm, int64_t n, int row_bytes,
+                                     const int32_t* __restrict__ adj, const unsigned char* __restrict__ posA,
+                                     int32_t* __restrict__ adjC, unsigned char* __restrict__ posAC) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = perm[i];
+        adjC[i] = adj[k];
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(posA + k * row_bytes);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(posAC + i * row_bytes);
+        for (int w = 0; w < row_bytes / 4; ++w) dst[w] = src[w];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Host orchestration
 // ---------------------------------------------------------------------------
@@ -806,13 +845,57 @@ std::vector<int32_t> host_conn(const fea_plan* p, cudaStream_t s) {
     return h;
 }
 
+// Per-node incidences in ascending (colour, element id) plus their position rows.
+void build_colour_incidences(fea_plan* p, const std::vector<int32_t>& colour_of_elem, cudaStream_t s) {
+    const int64_t n = p->n_adj;
+    const int row_bytes = p->pstride * p->pos_bytes;
+    p->adjC.alloc(n * 4 + 64);
+    p->posAC.alloc(n * row_bytes + 64);
+    FEA_CK(cudaMemsetAsync(p->posAC.p, 0, p->posAC.bytes, s));
+    if (n == 0) return;
+    // colour of every K row (kept elements; others never appear in the incidences)
+    std::vector<int32_t> kr(static_cast<size_t>(p->E));
+    if (p->E > 0)
+        FEA_CK(cudaMemcpy(kr.data(), p->elem_krow.p, kr.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> ck(static_cast<size_t>(p->krows()), 0);
+    int nc = 1;
+    for (int64_t le = 0; le < p->E; ++le) {
+        ck[kr[le]] = colour_of_elem[le];
+        nc = std::max(nc, colour_of_elem[le] + 1);
+    }
+    DevBuf d_ck, node_of, k1, v1, k2, v2;
+    d_ck.alloc(ck.size() * 4);
+    FEA_CK(cudaMemcpyAsync(d_ck.p, ck.data(), ck.size() * 4, cudaMemcpyHostToDevice, s));
+    node_of.alloc(n * 4);
+    k1.alloc(n * 4); v1.alloc(n * 4); k2.alloc(n * 4); v2.alloc(n * 4);
+    k_node_of<<<grid_for(p->n_own, 256), 256, 0, s>>>(p->adj_ptr.as<int64_t>(), p->n_own, node_of.as<int32_t>());
+    k_colour_keys<<<grid_for(n, 256), 256, 0, s>>>(p->adj.as<int32_t>(), n, p->npe, d_ck.as<int32_t>(),
+                                                   k1.as<uint32_t>(), v1.as<int32_t>());
+    FEA_CK(cudaGetLastError());
+    cub_call([&](void* t, size_t& tb) {  // pass 1: stable by colour
+        return cub::DeviceRadixSort::SortPairs(t, tb, k1.as<uint32_t>(), k2.as<uint32_t>(), v1.as<int32_t>(),
+                                               v2.as<int32_t>(), (int)n, 0, bits_for(static_cast<uint64_t>(nc)), s);
+    });
+    k_gather_keys<<<grid_for(n, 256), 256, 0, s>>>(node_of.as<int32_t>(), v2.as<int32_t>(), n, k1.as<uint32_t>());
+    FEA_CK(cudaGetLastError());
+    cub_call([&](void* t, size_t& tb) {  // pass 2: stable by node
+        return cub::DeviceRadixSort::SortPairs(t, tb, k1.as<uint32_t>(), k2.as<uint32_t>(), v2.as<int32_t>(),
+                                               v1.as<int32_t>(), (int)n, 0, bits_for(static_cast<uint64_t>(p->n_own)), s);
+    });
+    k_permute_incidences<<<grid_for(n, 256), 256, 0, s>>>(v1.as<int32_t>(), n, row_bytes, p->adj.as<int32_t>(),
+                                                          p->posA.as<unsigned char>(), p->adjC.as<int32_t>(),
+                                                          p->posAC.as<unsigned char>());
+    FEA_CK(cudaGetLastError());
+    FEA_CK(cudaStreamSynchronize(s));
+}
+
 }  // namespace
 
 int64_t metadata_bytes(const fea_plan* p) {
     return static_cast<int64_t>(p->conn_k.bytes + p->elem_id.bytes + p->elem_krow.bytes +
                                 p->adj_ptr.bytes + p->adj.bytes + p->nptr.bytes + p->ncol.bytes +
                                 p->nrun_ptr.bytes + p->posA.bytes + p->posE.bytes +
-                                p->order.bytes + p->colour_elems.bytes);
+                                p->order.bytes + p->colour_elems.bytes + p->adjC.bytes + p->posAC.bytes);
 }
 
 }  // namespace feagpu
@@ -1169,6 +1252,7 @@ fea_status fea_plan_set_colouring(fea_plan* p, const int32_t* colour_of) {
             FEA_CK(cudaMemcpy(p->colour_elems.p, by_colour.data(), by_colour.size() * 4,
                               cudaMemcpyHostToDevice));
         p->colour_off = off;
+        build_colour_incidences(p, col, st.s);
         p->has_colouring = true;
     });
 }

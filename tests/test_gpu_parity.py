@@ -79,6 +79,8 @@ def test_values_all_strategies(gpu, orc, mesh, n, d, perm):
         plan.set_colouring(gcol)
         got_c = plan.assemble(K, strategy="colour").cpu().numpy()
         assert got_c.tobytes() == want_col.tobytes()
+        got_p = plan.assemble(K, strategy="colour_passes").cpu().numpy()
+        assert got_p.tobytes() == want_col.tobytes()
         got_a = plan.assemble(K, strategy="atomic").cpu().numpy()
         assert close(got_a, want_seq)
 
@@ -96,13 +98,13 @@ def test_ones_bitwise_and_conservation(gpu, orc, mesh, n, d, perm):
     with gpu.Plan(ed, n_rows, dofs_per_node=d) as plan:
         col, _ = plan.greedy_colouring()
         plan.set_colouring(col)
-        for s in ("sorted", "atomic", "colour"):
+        for s in ("sorted", "atomic", "colour", "colour_passes"):
             got = plan.assemble(K, strategy=s).cpu().numpy()
             assert got.tobytes() == want.tobytes(), s
             assert got.sum() == E * m * m
 
 
-@pytest.mark.parametrize("strategy", ["sorted", "atomic", "colour"])
+@pytest.mark.parametrize("strategy", ["sorted", "atomic", "colour", "colour_passes"])
 def test_accumulate_twice_doubles(gpu, orc, strategy):
     """test_assembly.cpp:89-99: assembling twice without reset doubles every value."""
     import torch
@@ -267,6 +269,7 @@ def test_gpu_matches_reference_fixtures(gpu, orc, name):
         K = gpu.fill_seeded_k(E, m, 42)
         assert plan.assemble(K, strategy="sorted").cpu().numpy().tobytes() == g["values_seq"].tobytes()
         assert plan.assemble(K, strategy="colour").cpu().numpy().tobytes() == g["values_colour"].tobytes()
+        assert plan.assemble(K, strategy="colour_passes").cpu().numpy().tobytes() == g["values_colour"].tobytes()
         assert close(plan.assemble(K, strategy="atomic").cpu().numpy(), g["values_seq"])
         ones = torch.ones((E, m, m), dtype=torch.float64, device="cuda")
         for s in ("sorted", "atomic", "colour"):
