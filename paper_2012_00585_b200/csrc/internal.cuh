@@ -98,6 +98,7 @@ struct fea_plan {
     feagpu::DevBuf posA;      // PosT [n_adj*npe] positions, adjacency order (gather route)
     feagpu::DevBuf posE;      // PosT [E*npe*npe] positions, element order (atomic/colour routes; lazy)
     feagpu::DevBuf order;     // int32 [E] atomic-route element order (lazy)
+    feagpu::DevBuf node_order;  // int32 [n_own] gather traversal order (empty: node id order)
     // colouring
     bool has_colouring = false;
     feagpu::DevBuf colour_elems;           // int32 [E] local elements grouped by colour, ascending id

@@ -137,8 +137,9 @@ template <int G, int R, int PF, class PosT, bool DISTINCT>
 __global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
     k_gather_node(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
              const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
-             const int64_t* __restrict__ nptr, int64_t n_own, int d, int npe, int pstride,
-             int acc_stride, int pos_stride, int accumulate, double* __restrict__ values) {
+             const int64_t* __restrict__ nptr, const int32_t* __restrict__ order, int64_t n_own,
+             int d, int npe, int pstride, int acc_stride, int pos_stride, int accumulate,
+             int keep_k_in_l2, double* __restrict__ values) {
     extern __shared__ double sacc[];
     constexpr int GPW = 32 / G;
     const int m = d * npe;
@@ -166,10 +167,11 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
                           : 0u;
     }
 
-    const int64_t v = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * GPW + gw;
+    const int64_t vi = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * GPW + gw;
+    const int64_t v = (order != nullptr && vi < n_own) ? order[vi] : vi;
     int64_t b0 = 0, vb = 0;
     int n = 0, rowlen = 0, block = 0;
-    if (v < n_own) {
+    if (vi < n_own) {
         b0 = adj_ptr[v];
         n = static_cast<int>(adj_ptr[v + 1] - b0);
         const int64_t c0 = nptr[v];
@@ -206,7 +208,9 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int idx = r * G + gl;
-                if (idx < dm) kv[p][r] = ld_stream(src + idx);
+                // row blocks smaller than a 128 B line: keep lines in L2 for the element's
+                // other nodes (traversed close in time); else stream (read exactly once)
+                if (idx < dm) kv[p][r] = keep_k_in_l2 ? __ldcg(src + idx) : ld_stream(src + idx);
             }
         }
     };
@@ -648,8 +652,9 @@ void run_gather_node(fea_plan* p, const Incidences& in, const double* K, double*
     if (blocks == 0) return;
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
         K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const PosT*>(in.posA),
-        p->nptr.as<int64_t>(), p->n_own, p->d, p->npe, p->pstride, acc_stride, pos_stride,
-        accumulate ? 1 : 0, values);
+        p->nptr.as<int64_t>(), p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, p->d,
+        p->npe, p->pstride, acc_stride, pos_stride, accumulate ? 1 : 0, p->d * p->m * 8 < 128 ? 1 : 0,
+        values);
     FEA_CK(cudaGetLastError());
     p->last_launches += 1;
 }
@@ -659,7 +664,7 @@ void run_gather_node(fea_plan* p, const Incidences& in, const double* K, double*
 template <int G, int R, int PF, class PosT>
 void run_gather(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
                 cudaStream_t s) {
-    if (G == 32 && R >= 8) run_gather_stream<G, R, PF, PosT>(p, in, K, values, accumulate, s);
+    if (G == 32 && R >= 8 && !p->node_order.p) run_gather_stream<G, R, PF, PosT>(p, in, K, values, accumulate, s);
     else run_gather_node<G, R, PF, PosT>(p, in, K, values, accumulate, s);
 }
 
