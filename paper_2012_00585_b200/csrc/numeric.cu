@@ -45,6 +45,18 @@ unsigned grid_for(int64_t n, int threads) {
 
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 
+// Debug builds (-DFEA_DEBUG, tools/sanitize_case.py): trap on any out-of-range index.
+#ifdef FEA_DEBUG
+#define FEA_DCHECK(cond)     \
+    do {                     \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define FEA_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 // --- TMA bulk copy + mbarrier primitives (sm_90+/sm_100a PTX) ---------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -229,6 +241,7 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
                     const uint32_t t = tab[r];
                     q[r] = static_cast<int>(t & 1023u) * rowlen +
                            static_cast<int>(pk[(t >> 10) & 1023u]) * d + static_cast<int>(t >> 20);
+                    FEA_DCHECK(r * G + gl >= dm || (q[r] >= 0 && q[r] < block));
                 }
                 if (DISTINCT) {
                     // the slots of one element row block are distinct (no repeated node in
@@ -412,6 +425,7 @@ __global__ void __launch_bounds__(kWarps * 32, gather_min_blocks<R>())
                     const uint32_t tb = tab[r];
                     q[r] = static_cast<int>(tb & 1023u) * rowlen +
                            static_cast<int>(pk[(tb >> 10) & 1023u]) * d + static_cast<int>(tb >> 20);
+                    FEA_DCHECK(r * G + gl >= dm || (q[r] >= 0 && q[r] < block));
                 }
                 if (DISTINCT) {  // slots of one chunk are distinct: loads, adds, then stores
                     double a[R];
@@ -503,6 +517,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                 if (base >= 0) {
                     const int64_t s = base + static_cast<int64_t>(ki) * rl[a] +
                                       static_cast<int64_t>(pe[a * npe + b]) * d + kj;
+                    FEA_DCHECK(s >= base && s < base + static_cast<int64_t>(d) * rl[a]);
                     if (ATOMIC) atomicAdd(values + s, x);
                     else values[s] += x;
                 }
