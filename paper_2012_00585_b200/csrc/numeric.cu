@@ -459,6 +459,107 @@ __global__ void __launch_bounds__(kWarps * 32, gather_min_blocks<R>())
 }
 
 // ---------------------------------------------------------------------------
+// Deterministic gather, lane = column node (FEA_DET_SORTED; G >= npe, D = d compile-time)
+// ---------------------------------------------------------------------------
+// The d x d sub-block K[e][a*d+ki][b*d+kj] of an incident row block lands in the d x d block
+// of the node's values at column position pos(b): slot = ki*rowlen + pos(b)*d + kj. With lane
+// = column node b and the D*D rounds = (ki, kj) unrolled at compile time, each lane does ONE
+// position lookup per row block and every slot is a compile-time offset plus one add — the
+// per-entry decode of k_gather_node disappears. The strided K loads (lane b reads d
+// consecutive doubles of each of the d rows) go through L1 (ld.global.nc), which coalesces
+// them back into whole sectors; DRAM traffic is unchanged. Fold order per slot as in
+// k_gather_node: ascending element id, bit-identical to assemble_sequential.
+template <int G, int D, int PF, class PosT, bool DISTINCT>
+__global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
+    k_gather_cn(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
+                const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
+                const int64_t* __restrict__ nptr, const int32_t* __restrict__ order, int64_t n_own,
+                int npe, int pstride, int acc_stride, int pos_stride, int accumulate,
+                double* __restrict__ values) {
+    extern __shared__ double sacc[];
+    constexpr int GPW = 32 / G;
+    constexpr int R = D * D;
+    const int m = D * npe;
+    const int dm = D * m;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G;
+    const int gw = lane / G;
+    const int warp = threadIdx.x >> 5;
+    const int grp = warp * GPW + gw;
+    const bool col_ok = gl < npe;
+    double* acc = sacc + static_cast<int64_t>(grp) * acc_stride;
+    PosT* spos = reinterpret_cast<PosT*>(sacc + static_cast<int64_t>(kWarps) * GPW * acc_stride) +
+                 static_cast<int64_t>(grp) * pos_stride;
+
+    const int64_t vi = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * GPW + gw;
+    const int64_t v = (order != nullptr && vi < n_own) ? order[vi] : vi;
+    int64_t b0 = 0, vb = 0;
+    int n = 0, rowlen = 0, block = 0;
+    if (vi < n_own) {
+        b0 = adj_ptr[v];
+        n = static_cast<int>(adj_ptr[v + 1] - b0);
+        const int64_t c0 = nptr[v];
+        rowlen = static_cast<int>(D * (nptr[v + 1] - c0));
+        block = D * rowlen;
+        vb = static_cast<int64_t>(D) * D * c0;
+    }
+    const int32_t my_ent = gl < n ? adj[b0 + gl] : 0;
+    for (int q = gl; q < n * npe; q += G) {
+        const int k = q / npe;
+        spos[q] = posA[(b0 + k) * pstride + (q - k * npe)];
+    }
+    for (int i = gl; i < block; i += G) acc[i] = accumulate ? values[vb + i] : 0.0;
+    const int n_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
+    __syncwarp();
+
+    double kv[PF][R];
+    auto load = [&](int p, int k) {
+        const int32_t e0 = __shfl_sync(0xffffffffu, my_ent, (gw * G + (k & (G - 1))) & 31);
+        const int32_t entry = n <= G ? e0 : (k < n ? adj[b0 + k] : 0);
+        if (k < n && col_ok) {
+            const double* src = K + static_cast<int64_t>(entry) * dm + gl * D;
+#pragma unroll
+            for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+                for (int kj = 0; kj < D; ++kj) kv[p][ki * D + kj] = __ldg(src + ki * m + kj);
+        }
+    };
+#pragma unroll
+    for (int p = 0; p < PF; ++p) load(p, p);
+
+    for (int k0 = 0; k0 < n_max; k0 += PF) {
+#pragma unroll
+        for (int p = 0; p < PF; ++p) {
+            const int k = k0 + p;
+            if (k < n && col_ok) {
+                const int base = static_cast<int>(spos[k * npe + gl]) * D;
+                FEA_DCHECK(base + (D - 1) * rowlen + D - 1 < block);
+                if (DISTINCT) {
+                    double a[R];
+#pragma unroll
+                    for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+                        for (int kj = 0; kj < D; ++kj) a[ki * D + kj] = acc[ki * rowlen + base + kj];
+#pragma unroll
+                    for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+                        for (int kj = 0; kj < D; ++kj)
+                            acc[ki * rowlen + base + kj] = a[ki * D + kj] + kv[p][ki * D + kj];
+                } else {
+#pragma unroll
+                    for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+                        for (int kj = 0; kj < D; ++kj) acc[ki * rowlen + base + kj] += kv[p][ki * D + kj];
+                }
+            }
+            __syncwarp();
+            load(p, k + PF);
+        }
+    }
+    for (int i = gl; i < block; i += G) __stcs(values + vb + i, acc[i]);
+}
+
+// ---------------------------------------------------------------------------
 // Element-owner scatter: atomics (FEA_ATOMIC) or plain adds within a colour
 // ---------------------------------------------------------------------------
 // tab[idx] = a | ki<<8 | b<<16 | kj<<24 for idx = i*m + j, i = a*d+ki, j = b*d+kj.
@@ -683,10 +784,51 @@ void run_gather(fea_plan* p, const Incidences& in, const double* K, double* valu
     else run_gather_node<G, R, PF, PosT>(p, in, K, values, accumulate, s);
 }
 
+#ifndef FEA_CN_PF8
+#define FEA_CN_PF8 2
+#endif
+template <int G, int D, int PF, class PosT>
+void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
+                   cudaStream_t s) {
+    constexpr int GPW = 32 / G;
+    const int acc_stride = p->d * p->d * p->max_cnt + 1;
+    const int pos_stride = static_cast<int>((std::max<int64_t>(p->max_adj, 1) * p->npe + 7) & ~int64_t(7));
+    const size_t smem = static_cast<size_t>(kWarps) * GPW *
+                        (acc_stride * sizeof(double) + pos_stride * sizeof(PosT));
+    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
+    auto kern = p->dup_nodes ? k_gather_cn<G, D, PF, PosT, false> : k_gather_cn<G, D, PF, PosT, true>;
+    if (smem > 48 * 1024)
+        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t blocks = (p->n_own + kWarps * GPW - 1) / (kWarps * GPW);
+    if (blocks == 0) return;
+    kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
+        K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const PosT*>(in.posA), p->nptr.as<int64_t>(),
+        p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, p->npe, p->pstride, acc_stride,
+        pos_stride, accumulate ? 1 : 0, values);
+    FEA_CK(cudaGetLastError());
+    p->last_launches += 1;
+}
+
 template <class PosT>
 void gather(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
             cudaStream_t s) {
     const int dm = p->d * p->m;
+    // lane = column node (d in {2,3,4}, npe <= 32); measured faster than the decode-table
+    // kernels for every such shape
+    if (!p->cn_disabled && p->d >= 2 && p->d <= 4 && p->npe <= 32) {
+        const int G = p->npe <= 4 ? 4 : p->npe <= 8 ? 8 : p->npe <= 16 ? 16 : 32;
+        switch (G * 10 + p->d) {
+            case 42: return run_gather_cn<4, 2, 2, PosT>(p, in, K, values, accumulate, s);
+            case 43: return run_gather_cn<4, 3, 2, PosT>(p, in, K, values, accumulate, s);
+            case 44: return run_gather_cn<4, 4, 2, PosT>(p, in, K, values, accumulate, s);
+            case 82: return run_gather_cn<8, 2, 2, PosT>(p, in, K, values, accumulate, s);
+            case 83: return run_gather_cn<8, 3, FEA_CN_PF8, PosT>(p, in, K, values, accumulate, s);
+            case 84: return run_gather_cn<8, 4, 2, PosT>(p, in, K, values, accumulate, s);
+            case 163: return run_gather_cn<16, 3, 2, PosT>(p, in, K, values, accumulate, s);
+            case 323: return run_gather_cn<32, 3, 2, PosT>(p, in, K, values, accumulate, s);
+            default: break;
+        }
+    }
     if (dm <= 4) run_gather<4, 1, 8, PosT>(p, in, K, values, accumulate, s);
     else if (dm <= 8) run_gather<8, 1, 8, PosT>(p, in, K, values, accumulate, s);
     else if (dm <= 16) run_gather<16, 1, 4, PosT>(p, in, K, values, accumulate, s);

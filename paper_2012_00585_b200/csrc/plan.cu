@@ -984,6 +984,7 @@ fea_status fea_plan_create(int device, const int64_t* elem_dofs, int64_t n_eleme
         Stream st;
         auto p = std::make_unique<fea_plan>();
         p->device = device;
+        p->cn_disabled = std::getenv("FEA_GATHER_NO_CN") != nullptr;
         p->E_in = n_elements;
         p->m = m;
         p->n_rows = n_rows;
