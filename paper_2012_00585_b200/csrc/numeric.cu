@@ -469,8 +469,11 @@ __global__ void __launch_bounds__(kWarps * 32, gather_min_blocks<R>())
 // consecutive doubles of each of the d rows) go through L1 (ld.global.nc), which coalesces
 // them back into whole sectors; DRAM traffic is unchanged. Fold order per slot as in
 // k_gather_node: ascending element id, bit-identical to assemble_sequential.
+#ifndef FEA_CN_MINB
+#define FEA_CN_MINB 6
+#endif
 template <int G, int D, int PF, class PosT, bool DISTINCT>
-__global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
+__global__ void __launch_bounds__(kWarps * 32, FEA_CN_MINB)
     k_gather_cn(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
                 const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
                 const int64_t* __restrict__ nptr, const int32_t* __restrict__ order, int64_t n_own,
