@@ -204,6 +204,21 @@ FEA_API int32_t fea_plan_last_launches(const fea_plan* plan);
 FEA_API fea_status fea_fill_seeded_k(double* K, int64_t n, int32_t m, uint64_t seed,
                              const int64_t* elem_ids, void* stream);
 
+/*
+ * y = A x on an assembled matrix (the consumer of the assembly; CRAC's payoff).
+ * All pointers are DEVICE pointers; x is indexed by global column, y by (owned) row.
+ *  fea_spmv_csr : CSR arrays (row_ptr[n_rows+1], cols[nnz])
+ *  fea_spmv_crac: CRAC arrays (row_ptr[n_rows+1] in col_align entry units, col_align[2*runs+2])
+ *  fea_plan_spmv: the plan's own node-block layout (no column array needed)
+ * values is the fea_assemble output (identical for CSR and CRAC). Stream-ordered.
+ */
+FEA_API fea_status fea_spmv_csr(const int64_t* row_ptr, const int64_t* cols, const double* values,
+                                int64_t n_rows, const double* x, double* y, void* stream);
+FEA_API fea_status fea_spmv_crac(const int64_t* row_ptr, const int64_t* col_align, const double* values,
+                                 int64_t n_rows, const double* x, double* y, void* stream);
+FEA_API fea_status fea_plan_spmv(const fea_plan* plan, const double* values, const double* x, double* y,
+                                 void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,6 +57,9 @@ SIGNATURES = {
     "fea_plan_missing_entry": (c_int, [c_void_p, _P64, _P64, _P64]),
     "fea_plan_last_launches": (c_int32, [c_void_p]),
     "fea_fill_seeded_k": (c_int, [c_void_p, c_int64, c_int32, c_uint64, c_void_p, c_void_p]),
+    "fea_spmv_csr": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "fea_spmv_crac": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "fea_plan_spmv": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
 }
 
 _lib = None

@@ -198,6 +198,14 @@ class Plan:
                                                  _stream_ptr(stream)))
         return values_hosts
 
+    def spmv(self, values, x, y=None, stream=None):
+        """y = A x with the plan's node-block layout (device tensors; x over global columns)."""
+        import torch
+        if y is None:
+            y = torch.empty(self.n_rows, dtype=torch.float64, device=values.device)
+        _check(self._lib.fea_plan_spmv(self._h, _ptr(values), _ptr(x), _ptr(y), _stream_ptr(stream)))
+        return y
+
     def close(self) -> None:
         if self._h and self._h.value:
             self._lib.fea_plan_destroy(self._h)
@@ -229,3 +237,25 @@ def fill_seeded_k(n: int, m: int, seed: int, elem_ids=None, device: int = 0, out
     if ids is not None:
         torch.cuda.current_stream(out.device).synchronize()
     return out
+
+
+def spmv_csr(row_ptr, cols, values, x, y=None, stream=None):
+    """y = A x over device CSR arrays (int64 row_ptr/cols, fp64 values/x)."""
+    import torch
+    n = row_ptr.numel() - 1
+    if y is None:
+        y = torch.empty(n, dtype=torch.float64, device=values.device)
+    _check(N.lib().fea_spmv_csr(_ptr(row_ptr), _ptr(cols), _ptr(values), n, _ptr(x), _ptr(y),
+                                _stream_ptr(stream)))
+    return y
+
+
+def spmv_crac(crac_ptr, col_align, values, x, y=None, stream=None):
+    """y = A x over device CRAC arrays (row_ptr in col_align entry units, col_align pairs)."""
+    import torch
+    n = crac_ptr.numel() - 1
+    if y is None:
+        y = torch.empty(n, dtype=torch.float64, device=values.device)
+    _check(N.lib().fea_spmv_crac(_ptr(crac_ptr), _ptr(col_align), _ptr(values), n, _ptr(x), _ptr(y),
+                                 _stream_ptr(stream)))
+    return y

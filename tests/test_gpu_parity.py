@@ -297,3 +297,27 @@ def test_host_batch_pipeline(gpu, orc):
         plan.assemble_host_batch(Ks[:2], start, strategy="sorted", accumulate=True)
         for K, v in zip(Ks[:2], start):
             assert v.tobytes() == P.assemble_sequential(ed, K, np.full(P.nnz, 0.5)).tobytes()
+
+
+@pytest.mark.parametrize("mesh,n,d,perm", CASES)
+def test_spmv_csr_crac_nodes(gpu, orc, mesh, n, d, perm):
+    """y = A x through the CSR, CRAC and node-block kernels against a host CSR product
+    (different summation order than the host: |y - y_ref| <= 1e-12 * (|A| |x|) per row)."""
+    import torch
+    conn, nn, ed, n_rows = problem(mesh, n, d, perm)
+    with gpu.Plan(ed, n_rows, dofs_per_node=d) as plan:
+        K = gpu.fill_seeded_k(conn.shape[0], ed.shape[1], 3)
+        vals = plan.assemble(K, strategy="sorted")
+        rp, cs = plan.csr()
+        cp, ca = plan.crac()
+        x = np.random.default_rng(1).uniform(-1, 1, n_rows)
+        v = vals.cpu().numpy()
+        rows = np.repeat(np.arange(n_rows), np.diff(rp))
+        want = np.bincount(rows, weights=v * x[cs], minlength=n_rows)
+        scale = np.bincount(rows, weights=np.abs(v * x[cs]), minlength=n_rows)
+        xd = torch.from_numpy(x).cuda()
+        for got in (gpu.spmv_csr(torch.from_numpy(rp).cuda(), torch.from_numpy(cs).cuda(), vals, xd),
+                    gpu.spmv_crac(torch.from_numpy(cp).cuda(), torch.from_numpy(ca).cuda(), vals, xd),
+                    plan.spmv(vals, xd)):
+            g = got.cpu().numpy()
+            assert np.all(np.abs(g - want) <= 1e-12 * np.maximum(scale, 1e-300) + 1e-300)
