@@ -178,6 +178,13 @@ FEA_API fea_status fea_assemble(fea_plan* plan, const double* K, int32_t strateg
 FEA_API fea_status fea_assemble_host(fea_plan* plan, const double* K_host, int32_t strategy,
                              double* values_host, uint32_t flags, void* stream);
 
+/* Fused supplier: assemble the seeded synthetic element matrices of fea_fill_seeded_k WITHOUT
+ * materializing K — the gather kernels generate each entry in registers (the GPU form of the
+ * reference's ElementMatrixSupplier called inside the assembly, assembly.hpp:37, :78). Same bits
+ * as fea_assemble on a fea_fill_seeded_k buffer. Strategies FEA_DET_SORTED / FEA_DET_COLOUR. */
+FEA_API fea_status fea_assemble_seeded(fea_plan* plan, uint64_t seed, int32_t strategy, double* values,
+                                       uint32_t flags, void* stream);
+
 /* Repeated end-to-end assemblies of the same plan with new element matrices (Newton
  * iterations, time steps, load cases): n_steps pairs of HOST buffers K_hosts[i] ->
  * values_hosts[i]. Pipelined with two device staging slots: step i's K host->device copy

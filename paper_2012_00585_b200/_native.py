@@ -56,6 +56,7 @@ SIGNATURES = {
                                         c_int32, c_uint32, c_void_p]),
     "fea_plan_missing_entry": (c_int, [c_void_p, _P64, _P64, _P64]),
     "fea_plan_last_launches": (c_int32, [c_void_p]),
+    "fea_assemble_seeded": (c_int, [c_void_p, c_uint64, c_int32, c_void_p, c_uint32, c_void_p]),
     "fea_fill_seeded_k": (c_int, [c_void_p, c_int64, c_int32, c_uint64, c_void_p, c_void_p]),
     "fea_spmv_csr": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "fea_spmv_crac": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),

@@ -174,6 +174,18 @@ class Plan:
                                       _stream_ptr(stream)))
         return values
 
+    def assemble_seeded(self, seed: int, values=None, strategy: str = "sorted", accumulate: bool = False,
+                        stream=None):
+        """Fused supplier: assemble the seeded element matrices generated inside the kernel."""
+        import torch
+        if values is None:
+            values = torch.zeros(self.nnz, dtype=torch.float64, device=f"cuda:{self.device}")
+            accumulate = False
+        flags = (N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE) | _EXTRA_FLAGS.get(strategy, 0)
+        _check(self._lib.fea_assemble_seeded(self._h, ctypes.c_uint64(seed), STRATEGIES[strategy],
+                                             _ptr(values), flags, _stream_ptr(stream)))
+        return values
+
     def assemble_host(self, K_host, values_host=None, strategy: str = "sorted",
                       accumulate: bool = False, stream=None):
         """End-to-end form: host K in, host values out (H2D + assemble + D2H, synchronous)."""

@@ -108,6 +108,8 @@ struct fea_plan {
     int64_t miss_e = -1, miss_r = -1, miss_c = -1;
     // bookkeeping
     int32_t last_launches = 0;
+    bool gen_on = false;       // fea_assemble_seeded in progress: kernels generate K
+    uint64_t gen_seed = 0;
     bool cn_disabled = false;  // FEA_GATHER_NO_CN=1: decode-table gather (A/B)
     feagpu::DevBuf stage_K, stage_V;       // fea_assemble_host staging
     feagpu::DevBuf bstage_K[2], bstage_V[2];  // fea_assemble_host_batch double buffers

@@ -57,6 +57,35 @@ __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p);
     } while (0)
 #endif
 
+// Seeded element-matrix generator (the counter-hash supplier): the same bits
+// as oracle/oracle.c orc_kval. kgen_elem is hoisted per element, kgen_entry per entry.
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    uint64_t z = x + 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t kgen_elem(uint64_t seed, int64_t id) {
+    return mix64(seed + static_cast<uint64_t>(id));
+}
+__device__ __forceinline__ double kgen_entry(uint64_t he, int i, int j) {
+    const uint64_t lo = static_cast<uint64_t>(i < j ? i : j);
+    const uint64_t hi = static_cast<uint64_t>(i < j ? j : i);
+    const uint64_t h = mix64(he ^ ((lo << 32) | hi));
+    return static_cast<double>(h >> 11) * 0x1p-53 * 2.0 - 1.0;
+}
+__device__ __forceinline__ double kval(uint64_t seed, int64_t e, int i, int j) {
+    return kgen_entry(kgen_elem(seed, e), i, j);
+}
+
+// Fused supplier: when on, the gather kernels generate K[e][i][j] in registers instead of
+// reading it (fea_assemble_seeded) — no 8*E*m^2 bytes of K traffic.
+struct GenK {
+    int on;
+    uint64_t seed;
+    const int64_t* ids;  // element id per K row (nullptr: the K row is the element id)
+};
+
 // --- TMA bulk copy + mbarrier primitives (sm_90+/sm_100a PTX) ---------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -145,13 +174,13 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // (coalesced, into registers / shared memory) so no dependent global load sits
 // between two row-block loads. Kept lean in registers: occupancy (many warps,
 // each with a few KB in flight) is what saturates HBM on this random-block gather.
-template <int G, int R, int PF, class PosT, bool DISTINCT>
+template <int G, int R, int PF, class PosT, bool DISTINCT, bool GEN>
 __global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
     k_gather_node(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
              const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
              const int64_t* __restrict__ nptr, const int32_t* __restrict__ order, int64_t n_own,
              int d, int npe, int pstride, int acc_stride, int pos_stride, int accumulate,
-             int keep_k_in_l2, double* __restrict__ values) {
+             int keep_k_in_l2, GenK gen, double* __restrict__ values) {
     extern __shared__ double sacc[];
     constexpr int GPW = 32 / G;
     const int m = d * npe;
@@ -216,13 +245,28 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
     auto load = [&](int p, int k) {
         const int32_t entry = entry_of(k);
         if (k < n) {
-            const double* src = K + static_cast<int64_t>(entry) * dm;
+            if (GEN) {  // fused supplier
+                const int64_t krow = entry / npe;
+                const int a = static_cast<int>(entry - krow * npe);
+                const uint64_t he = kgen_elem(gen.seed, gen.ids ? gen.ids[krow] : krow);
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int idx = r * G + gl;
-                // row blocks smaller than a 128 B line: keep lines in L2 for the element's
-                // other nodes (traversed close in time); else stream (read exactly once)
-                if (idx < dm) kv[p][r] = keep_k_in_l2 ? __ldcg(src + idx) : ld_stream(src + idx);
+                for (int r = 0; r < R; ++r) {
+                    const int idx = r * G + gl;
+                    if (idx < dm) {
+                        const uint32_t t = tab[r];
+                        kv[p][r] = kgen_entry(he, a * d + static_cast<int>(t & 1023u),
+                                              static_cast<int>((t >> 10) & 1023u) * d + static_cast<int>(t >> 20));
+                    }
+                }
+            } else {
+                const double* src = K + static_cast<int64_t>(entry) * dm;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int idx = r * G + gl;
+                    // row blocks smaller than a 128 B line: keep lines in L2 for the element's
+                    // other nodes (traversed close in time); else stream (read exactly once)
+                    if (idx < dm) kv[p][r] = keep_k_in_l2 ? __ldcg(src + idx) : ld_stream(src + idx);
+                }
             }
         }
     };
@@ -472,12 +516,12 @@ __global__ void __launch_bounds__(kWarps * 32, gather_min_blocks<R>())
 #ifndef FEA_CN_MINB
 #define FEA_CN_MINB 6
 #endif
-template <int G, int D, int PF, class PosT, bool DISTINCT>
+template <int G, int D, int PF, class PosT, bool DISTINCT, bool GEN>
 __global__ void __launch_bounds__(kWarps * 32, FEA_CN_MINB)
     k_gather_cn(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
                 const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
                 const int64_t* __restrict__ nptr, const int32_t* __restrict__ order, int64_t n_own,
-                int npe, int pstride, int acc_stride, int pos_stride, int accumulate,
+                int npe, int pstride, int acc_stride, int pos_stride, int accumulate, GenK gen,
                 double* __restrict__ values) {
     extern __shared__ double sacc[];
     constexpr int GPW = 32 / G;
@@ -520,11 +564,21 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_CN_MINB)
         const int32_t e0 = __shfl_sync(0xffffffffu, my_ent, (gw * G + (k & (G - 1))) & 31);
         const int32_t entry = n <= G ? e0 : (k < n ? adj[b0 + k] : 0);
         if (k < n && col_ok) {
-            const double* src = K + static_cast<int64_t>(entry) * dm + gl * D;
+            if (GEN) {  // fused supplier: generate the d x d sub-block in registers
+                const int64_t krow = entry / npe;
+                const int a = static_cast<int>(entry - krow * npe);
+                const uint64_t he = kgen_elem(gen.seed, gen.ids ? gen.ids[krow] : krow);
 #pragma unroll
-            for (int ki = 0; ki < D; ++ki)
+                for (int ki = 0; ki < D; ++ki)
 #pragma unroll
-                for (int kj = 0; kj < D; ++kj) kv[p][ki * D + kj] = __ldg(src + ki * m + kj);
+                    for (int kj = 0; kj < D; ++kj) kv[p][ki * D + kj] = kgen_entry(he, a * D + ki, gl * D + kj);
+            } else {
+                const double* src = K + static_cast<int64_t>(entry) * dm + gl * D;
+#pragma unroll
+                for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+                    for (int kj = 0; kj < D; ++kj) kv[p][ki * D + kj] = __ldg(src + ki * m + kj);
+            }
         }
     };
 #pragma unroll
@@ -685,19 +739,6 @@ __global__ void k_iota32(int32_t* x, int64_t n) {
         x[i] = static_cast<int32_t>(i);
 }
 
-__device__ __forceinline__ double kval(uint64_t seed, int64_t e, int i, int j) {
-    auto mix = [](uint64_t x) {
-        uint64_t z = x + 0x9e3779b97f4a7c15ULL;
-        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-        return z ^ (z >> 31);
-    };
-    const uint64_t lo = static_cast<uint64_t>(i < j ? i : j);
-    const uint64_t hi = static_cast<uint64_t>(i < j ? j : i);
-    const uint64_t h = mix(mix(seed + static_cast<uint64_t>(e)) ^ ((lo << 32) | hi));
-    return static_cast<double>(h >> 11) * 0x1p-53 * 2.0 - 1.0;
-}
-
 __global__ void k_fill_k(double* __restrict__ K, int64_t n, int m, uint64_t seed,
                          const int64_t* __restrict__ ids) {
     const int64_t mm = static_cast<int64_t>(m) * m;
@@ -721,6 +762,14 @@ void cub_call(F&& f) {
 }
 
 // --- launch helpers --------------------------------------------------------
+
+GenK gen_of(const fea_plan* p) {
+    GenK g{};
+    g.on = p->gen_on ? 1 : 0;
+    g.seed = p->gen_seed;
+    g.ids = (p->k_compact && p->partitioned) ? p->elem_id.as<int64_t>() : nullptr;
+    return g;
+}
 
 template <int G, int R, int PF, class PosT>
 void run_gather_stream(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
@@ -763,7 +812,10 @@ void run_gather_node(fea_plan* p, const Incidences& in, const double* K, double*
                   (acc_stride * sizeof(double) + pos_stride * sizeof(PosT));
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID,
                 "node row block too large for shared-memory accumulation");
-    auto kern = p->dup_nodes ? k_gather_node<G, R, PF, PosT, false> : k_gather_node<G, R, PF, PosT, true>;
+    auto kern = p->gen_on ? (p->dup_nodes ? k_gather_node<G, R, PF, PosT, false, true>
+                                          : k_gather_node<G, R, PF, PosT, true, true>)
+                          : (p->dup_nodes ? k_gather_node<G, R, PF, PosT, false, false>
+                                          : k_gather_node<G, R, PF, PosT, true, false>);
     if (smem > 48 * 1024)
         FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t groups = p->n_own;
@@ -773,7 +825,7 @@ void run_gather_node(fea_plan* p, const Incidences& in, const double* K, double*
         K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const PosT*>(in.posA),
         p->nptr.as<int64_t>(), p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, p->d,
         p->npe, p->pstride, acc_stride, pos_stride, accumulate ? 1 : 0, p->d * p->m * 8 < 128 ? 1 : 0,
-        values);
+        gen_of(p), values);
     FEA_CK(cudaGetLastError());
     p->last_launches += 1;
 }
@@ -783,7 +835,7 @@ void run_gather_node(fea_plan* p, const Incidences& in, const double* K, double*
 template <int G, int R, int PF, class PosT>
 void run_gather(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
                 cudaStream_t s) {
-    if (G == 32 && R >= 8 && !p->node_order.p) run_gather_stream<G, R, PF, PosT>(p, in, K, values, accumulate, s);
+    if (G == 32 && R >= 8 && !p->node_order.p && !p->gen_on) run_gather_stream<G, R, PF, PosT>(p, in, K, values, accumulate, s);
     else run_gather_node<G, R, PF, PosT>(p, in, K, values, accumulate, s);
 }
 
@@ -799,7 +851,10 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
     const size_t smem = static_cast<size_t>(kWarps) * GPW *
                         (acc_stride * sizeof(double) + pos_stride * sizeof(PosT));
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
-    auto kern = p->dup_nodes ? k_gather_cn<G, D, PF, PosT, false> : k_gather_cn<G, D, PF, PosT, true>;
+    auto kern = p->gen_on ? (p->dup_nodes ? k_gather_cn<G, D, PF, PosT, false, true>
+                                          : k_gather_cn<G, D, PF, PosT, true, true>)
+                          : (p->dup_nodes ? k_gather_cn<G, D, PF, PosT, false, false>
+                                          : k_gather_cn<G, D, PF, PosT, true, false>);
     if (smem > 48 * 1024)
         FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t blocks = (p->n_own + kWarps * GPW - 1) / (kWarps * GPW);
@@ -807,7 +862,7 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
         K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const PosT*>(in.posA), p->nptr.as<int64_t>(),
         p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, p->npe, p->pstride, acc_stride,
-        pos_stride, accumulate ? 1 : 0, values);
+        pos_stride, accumulate ? 1 : 0, gen_of(p), values);
     FEA_CK(cudaGetLastError());
     p->last_launches += 1;
 }
@@ -950,7 +1005,7 @@ void assemble(fea_plan* p, const double* K, int strategy, double* values, uint32
         throw Error(FEA_ERR_MISSING_ENTRY, buf);
     }
     FEA_REQUIRE(p->nnz == 0 || values, FEA_ERR_INVALID, "values is NULL");
-    FEA_REQUIRE(p->E == 0 || K, FEA_ERR_INVALID, "K is NULL");
+    FEA_REQUIRE(p->E == 0 || K || p->gen_on, FEA_ERR_INVALID, "K is NULL");
     const bool overwrite = (flags & FEA_OVERWRITE) != 0;
     p->last_launches = 0;
     if (strategy == FEA_DET_COLOUR)
@@ -1102,6 +1157,26 @@ fea_status fea_assemble_host_batch(fea_plan* plan, const double* const* K_hosts,
         cudaStreamDestroy(sin);
         cudaStreamDestroy(sout);
         plan->last_launches = launches;
+    });
+}
+
+fea_status fea_assemble_seeded(fea_plan* plan, uint64_t seed, int32_t strategy, double* values,
+                               uint32_t flags, void* stream) {
+    return guarded_n([&] {
+        FEA_REQUIRE(plan, FEA_ERR_INVALID, "plan is NULL");
+        FEA_REQUIRE(strategy == FEA_DET_SORTED || (strategy == FEA_DET_COLOUR && !(flags & FEA_COLOUR_PASSES)),
+                    FEA_ERR_INVALID, "the fused supplier runs in the segmented-reduction routes "
+                                     "(FEA_DET_SORTED, FEA_DET_COLOUR)");
+        DeviceScope ds(plan->device);
+        plan->gen_on = true;
+        plan->gen_seed = seed;
+        try {
+            assemble(plan, nullptr, strategy, values, flags, static_cast<cudaStream_t>(stream));
+        } catch (...) {
+            plan->gen_on = false;
+            throw;
+        }
+        plan->gen_on = false;
     });
 }
 

@@ -321,3 +321,28 @@ def test_spmv_csr_crac_nodes(gpu, orc, mesh, n, d, perm):
                     plan.spmv(vals, xd)):
             g = got.cpu().numpy()
             assert np.all(np.abs(g - want) <= 1e-12 * np.maximum(scale, 1e-300) + 1e-300)
+
+
+@pytest.mark.parametrize("mesh,n,d,perm", CASES)
+def test_fused_supplier_bitwise(gpu, mesh, n, d, perm):
+    """fea_assemble_seeded (K generated inside the gather) == fea_assemble on a materialized seeded K."""
+    conn, nn, ed, n_rows = problem(mesh, n, d, perm)
+    with gpu.Plan(ed, n_rows, dofs_per_node=d) as plan:
+        K = gpu.fill_seeded_k(conn.shape[0], ed.shape[1], 11)
+        want = plan.assemble(K, strategy="sorted")
+        got = plan.assemble_seeded(11, strategy="sorted")
+        assert got.cpu().numpy().tobytes() == want.cpu().numpy().tobytes()
+        plan.set_colouring(plan.greedy_colouring()[0])
+        assert plan.assemble_seeded(11, strategy="colour").cpu().numpy().tobytes() == \
+            plan.assemble(K, strategy="colour").cpu().numpy().tobytes()
+
+
+def test_fused_supplier_partitioned_compact(gpu):
+    conn, nn, ed, n_rows = problem("hex8", 4, 3, "elements")
+    with gpu.Plan(ed, n_rows, dofs_per_node=3) as full:
+        want = full.assemble_seeded(5).cpu().numpy()
+        rp, _ = full.csr()
+    rb, re = 3 * 40, 3 * 90
+    with gpu.Plan(ed, n_rows, dofs_per_node=3, row_range=(rb, re), k_compact=True) as plan:
+        got = plan.assemble_seeded(5).cpu().numpy()
+        assert got.tobytes() == want[rp[rb]:rp[re]].tobytes()
