@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libfea_gpu.so"
-SOURCES = ["plan.cu", "numeric.cu", "spmv.cu"]
+SOURCES = ["plan.cu", "numeric.cu", "gather_u8.cu", "gather_u16.cu", "spmv.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-fvisibility=hidden", "-Xptxas", "-v",
@@ -38,18 +38,22 @@ def build(verbose: bool = False, force: bool = False, out: Path | None = None,
         return lib
     objdir = PKG / ("_build" if out is None else "_build_" + lib.stem)
     objdir.mkdir(exist_ok=True)
-    objs = []
-    for s in SOURCES:
-        obj = objdir / (Path(s).stem + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, *defines, "-c", str(CSRC / s), "-o", str(obj)]
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src: str) -> str:
+        obj = objdir / (Path(src).stem + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *defines, "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed on {s}")
+            raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
             sys.stderr.write(r.stderr)
-        (objdir / (Path(s).stem + ".ptxas.txt")).write_text(r.stderr)
-        objs.append(str(obj))
+        (objdir / (Path(src).stem + ".ptxas.txt")).write_text(r.stderr)
+        return str(obj)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
     tmp = lib.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)

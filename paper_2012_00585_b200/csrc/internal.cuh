@@ -118,6 +118,21 @@ struct fea_plan {
 };
 
 namespace feagpu {
+// Per-node incidence order used by the gather: ascending element id (FEA_DET_SORTED) or
+// ascending (colour, element id) (FEA_DET_COLOUR), with the matching position rows.
+struct Incidences {
+    const int32_t* adj;
+    const void* posA;
+};
+// gather_u8.cu / gather_u16.cu (numeric kernels per position width)
+void gather_u8(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
+               cudaStream_t s);
+void gather_u16(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
+                cudaStream_t s);
+void scatter_u8(fea_plan* p, const double* K, const int32_t* list, int64_t n_list, double* values,
+                bool atomic, cudaStream_t s);
+void scatter_u16(fea_plan* p, const double* K, const int32_t* list, int64_t n_list, double* values,
+                 bool atomic, cudaStream_t s);
 // numeric.cu
 void ensure_element_maps(fea_plan* p, cudaStream_t s);
 void assemble(fea_plan* p, const double* K, int strategy, double* values, uint32_t flags,

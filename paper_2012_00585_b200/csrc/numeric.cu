@@ -1,937 +1,23 @@
-// Numeric phase of the B200 FE-assembly library (north-star subsystem 3):
-// the scatter-add G(D(r), D(c)) += K_e(r, c) of scatter_element
-// (assembly.hpp:77-92) for all elements, with three conflict strategies.
+// Numeric phase of the B200 FE-assembly library (north-star subsystem 3): the scatter-add
+// G(D(r), D(c)) += K_e(r, c) of scatter_element (assembly.hpp:77-92) for all elements, with
+// three conflict strategies (kernels in kernels.cuh, instantiated per position width in
+// gather_u8.cu / gather_u16.cu):
 //
-//  FEA_DET_SORTED  k_gather   — owner-computes segmented reduction. One lane
-//      group owns a node's d rows (a contiguous block of values); it streams
-//      the node's incident element-matrix row blocks K[e][a*d .. a*d+d-1][:]
-//      (d*m contiguous doubles each) in ascending element id and folds them
-//      into a shared-memory copy of the block, then writes the block once.
-//      Per slot this is a left fold from the slot's start value in ascending
-//      element order: bit-identical to assemble_sequential (assembly.hpp:112).
-//      Every K byte is read once, every value written once, no atomics.
-//  FEA_ATOMIC      k_scatter<true>  — element owner, one fp64 atomicAdd
-//      (RED.E.ADD.F64) per entry, elements visited in a locality order
-//      (assemble_atomic, assembly.hpp:121-126).
-//  FEA_DET_COLOUR  k_scatter<false> — one launch per colour, plain
-//      load-add-store (assemble_coloured_vectorized, assembly.hpp:175-195).
-#include <cub/cub.cuh>
-
-#include <cstring>
-#include <string>
-
-#include "internal.cuh"
+//  FEA_DET_SORTED  owner-computes segmented reduction (k_gather_cn / k_gather_node /
+//      k_gather_stream). A lane group owns a node's d rows (a contiguous block of values); it
+//      streams the node's incident element-matrix row blocks K[e][a*d .. a*d+d-1][:] in
+//      ascending element id and folds them into a shared-memory copy of the block, then writes
+//      the block once. Per slot: a left fold from the slot's start value in ascending element
+//      order — bit-identical to assemble_sequential (assembly.hpp:112-118). K read once, values
+//      written once, no atomics.
+//  FEA_DET_COLOUR  the same reduction over incidences ordered by (colour, element): per slot
+//      the colour order of assemble_coloured_vectorized (assembly.hpp:175-195), bit-identical;
+//      FEA_COLOUR_PASSES runs it literally, one k_scatter<plain> launch per colour.
+//  FEA_ATOMIC      k_scatter<atomic>: element owner, one fp64 atomicAdd (RED.E.ADD.F64) per
+//      entry, elements in a locality order (assemble_atomic, assembly.hpp:121-126).
+#include "kernels.cuh"
 
 namespace feagpu {
-extern thread_local std::string g_err;
-
-namespace {
-
-constexpr int kWarps = 4;  // warps per CTA for the numeric kernels
-
-// Per-node incidence order used by the gather: ascending element id (FEA_DET_SORTED) or
-// ascending (colour, element id) (FEA_DET_COLOUR), with the matching position rows.
-struct Incidences {
-    const int32_t* adj;
-    const void* posA;
-};
-
-unsigned grid_for(int64_t n, int threads) {
-    int64_t b = (n + threads - 1) / threads;
-    if (b < 1) b = 1;
-    if (b > 148 * 64) b = 148 * 64;
-    return static_cast<unsigned>(b);
-}
-
-__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
-
-// Debug builds (-DFEA_DEBUG, tools/sanitize_case.py): trap on any out-of-range index.
-#ifdef FEA_DEBUG
-#define FEA_DCHECK(cond)     \
-    do {                     \
-        if (!(cond)) __trap(); \
-    } while (0)
-#else
-#define FEA_DCHECK(cond) \
-    do {                 \
-    } while (0)
-#endif
-
-// Seeded element-matrix generator (the counter-hash supplier): the same bits
-// as oracle/oracle.c orc_kval. kgen_elem is hoisted per element, kgen_entry per entry.
-__device__ __forceinline__ uint64_t mix64(uint64_t x) {
-    uint64_t z = x + 0x9e3779b97f4a7c15ULL;
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-    return z ^ (z >> 31);
-}
-__device__ __forceinline__ uint64_t kgen_elem(uint64_t seed, int64_t id) {
-    return mix64(seed + static_cast<uint64_t>(id));
-}
-__device__ __forceinline__ double kgen_entry(uint64_t he, int i, int j) {
-    const uint64_t lo = static_cast<uint64_t>(i < j ? i : j);
-    const uint64_t hi = static_cast<uint64_t>(i < j ? j : i);
-    const uint64_t h = mix64(he ^ ((lo << 32) | hi));
-    return static_cast<double>(h >> 11) * 0x1p-53 * 2.0 - 1.0;
-}
-__device__ __forceinline__ double kval(uint64_t seed, int64_t e, int i, int j) {
-    return kgen_entry(kgen_elem(seed, e), i, j);
-}
-
-// Fused supplier: when on, the gather kernels generate K[e][i][j] in registers instead of
-// reading it (fea_assemble_seeded) — no 8*E*m^2 bytes of K traffic.
-struct GenK {
-    int on;
-    uint64_t seed;
-    const int64_t* ids;  // element id per K row (nullptr: the K row is the element id)
-};
-
-// --- TMA bulk copy + mbarrier primitives (sm_90+/sm_100a PTX) ---------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "LAB_WAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@P1 bra DONE;\n"
-        "bra LAB_WAIT;\n"
-        "DONE:\n"
-        "}\n" ::"r"(bar),
-        "r"(phase)
-        : "memory");
-}
-// 1D bulk copy global -> shared (TMA, SASS UBLKCP), completion via mbarrier tx bytes;
-// L2 evict-first: each K byte is read exactly once.
-__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes,
-                                            uint32_t bar, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-        "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
-        "l"(src), "r"(bytes), "r"(bar), "l"(policy)
-        : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-// Ampere-style async copy global -> shared (SASS LDGSTS), 8 or 16 bytes per lane,
-// bypassing registers; completion tracked by an mbarrier (cp.async.mbarrier.arrive).
-template <int UNIT>
-__device__ __forceinline__ void cp_async(uint32_t dst, uint64_t src) {
-    if constexpr (UNIT == 16)
-        asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-    else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-#ifndef FEA_GATHER_MIN_BLOCKS
-#define FEA_GATHER_MIN_BLOCKS 5
-#endif
-#ifndef FEA_GATHER_MIN_BLOCKS_WIDE
-#define FEA_GATHER_MIN_BLOCKS_WIDE 4
-#endif
-// ---------------------------------------------------------------------------
-// Deterministic owner-computes gather, one node per lane group (FEA_DET_SORTED)
-// ---------------------------------------------------------------------------
-// A group of G lanes owns one node: the node's d rows are one contiguous block of
-// values. The group streams the node's incident element-matrix row blocks
-// K[e][a*d..a*d+d-1][:] (d*m contiguous doubles each, one per incident element,
-// ascending element id) straight into registers — R rounds of G entries per
-// block, PF blocks in flight — and folds them into a shared-memory copy of the
-// node block (one __syncwarp between blocks), then writes the block once with
-// coalesced streaming stores. Per slot this is a left fold from the slot's
-// start value in ascending element order: bit-identical to assemble_sequential
-// (assembly.hpp:112-118). K is read once, values written once, no atomics.
-// The node's incidence list and position-map slice are loaded once per node
-// (coalesced, into registers / shared memory) so no dependent global load sits
-// between two row-block loads. Kept lean in registers: occupancy (many warps,
-// each with a few KB in flight) is what saturates HBM on this random-block gather.
-template <int G, int R, int PF, class PosT, bool DISTINCT, bool GEN>
-__global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
-    k_gather_node(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
-             const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
-             const int64_t* __restrict__ nptr, const int32_t* __restrict__ order, int64_t n_own,
-             int d, int npe, int pstride, int acc_stride, int pos_stride, int accumulate,
-             int keep_k_in_l2, GenK gen, double* __restrict__ values) {
-    extern __shared__ double sacc[];
-    constexpr int GPW = 32 / G;
-    const int m = d * npe;
-    const int dm = d * m;
-    const int lane = threadIdx.x & 31;
-    const int gl = lane % G;
-    const int gw = lane / G;
-    const int warp = threadIdx.x >> 5;
-    const int grp = warp * GPW + gw;
-    double* acc = sacc + static_cast<int64_t>(grp) * acc_stride;
-    PosT* spos = reinterpret_cast<PosT*>(sacc + static_cast<int64_t>(kWarps) * GPW * acc_stride) +
-                 static_cast<int64_t>(grp) * pos_stride;
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
-
-    // chunk-independent decode of this lane's entries, packed ki | b<<10 | kj<<20
-    uint32_t tab[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int idx = r * G + gl;
-        const int ki = idx / m;
-        const int j = idx - ki * m;
-        const int b = j / d;
-        tab[r] = idx < dm ? (static_cast<uint32_t>(ki) | (static_cast<uint32_t>(b) << 10) |
-                             (static_cast<uint32_t>(j - b * d) << 20))
-                          : 0u;
-    }
-
-    const int64_t vi = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * GPW + gw;
-    const int64_t v = (order != nullptr && vi < n_own) ? order[vi] : vi;
-    int64_t b0 = 0, vb = 0;
-    int n = 0, rowlen = 0, block = 0;
-    if (vi < n_own) {
-        b0 = adj_ptr[v];
-        n = static_cast<int>(adj_ptr[v + 1] - b0);
-        const int64_t c0 = nptr[v];
-        rowlen = static_cast<int>(d * (nptr[v + 1] - c0));
-        block = d * rowlen;
-        vb = static_cast<int64_t>(d) * d * c0;
-    }
-    // the node's incidences (lane gl holds entry gl when n <= G) and position slice
-    const int32_t my_ent = gl < n ? adj[b0 + gl] : 0;
-    {
-        const int np = n * npe;
-        for (int q = gl; q < np; q += G) {
-            const int k = q / npe;
-            spos[q] = posA[(b0 + k) * pstride + (q - k * npe)];
-        }
-    }
-    if (accumulate) {
-        for (int i = gl; i < block; i += G) acc[i] = values[vb + i];
-    } else {
-        for (int i = gl; i < block; i += G) acc[i] = 0.0;
-    }
-    const int n_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
-    __syncwarp();
-
-    double kv[PF][R];
-    auto entry_of = [&](int k) -> int32_t {
-        const int32_t e = __shfl_sync(0xffffffffu, my_ent, (gw * G + (k & (G - 1))) & 31);
-        return n <= G ? e : (k < n ? adj[b0 + k] : 0);
-    };
-    auto load = [&](int p, int k) {
-        const int32_t entry = entry_of(k);
-        if (k < n) {
-            if (GEN) {  // fused supplier
-                const int64_t krow = entry / npe;
-                const int a = static_cast<int>(entry - krow * npe);
-                const uint64_t he = kgen_elem(gen.seed, gen.ids ? gen.ids[krow] : krow);
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const int idx = r * G + gl;
-                    if (idx < dm) {
-                        const uint32_t t = tab[r];
-                        kv[p][r] = kgen_entry(he, a * d + static_cast<int>(t & 1023u),
-                                              static_cast<int>((t >> 10) & 1023u) * d + static_cast<int>(t >> 20));
-                    }
-                }
-            } else {
-                const double* src = K + static_cast<int64_t>(entry) * dm;
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const int idx = r * G + gl;
-                    // row blocks smaller than a 128 B line: keep lines in L2 for the element's
-                    // other nodes (traversed close in time); else stream (read exactly once)
-                    if (idx < dm) kv[p][r] = keep_k_in_l2 ? __ldcg(src + idx) : ld_stream(src + idx);
-                }
-            }
-        }
-    };
-#pragma unroll
-    for (int p = 0; p < PF; ++p) load(p, p);
-
-    for (int k0 = 0; k0 < n_max; k0 += PF) {
-#pragma unroll
-        for (int p = 0; p < PF; ++p) {
-            const int k = k0 + p;
-            if (k < n) {
-                const PosT* pk = spos + k * npe;
-                int q[R];
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const uint32_t t = tab[r];
-                    q[r] = static_cast<int>(t & 1023u) * rowlen +
-                           static_cast<int>(pk[(t >> 10) & 1023u]) * d + static_cast<int>(t >> 20);
-                    FEA_DCHECK(r * G + gl >= dm || (q[r] >= 0 && q[r] < block));
-                }
-                if (DISTINCT) {
-                    // the slots of one element row block are distinct (no repeated node in
-                    // an element): all loads, then all adds, then all stores
-                    double a[R];
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (r * G + gl < dm) a[r] = acc[q[r]];
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (r * G + gl < dm) acc[q[r]] = a[r] + kv[p][r];
-                } else {
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (r * G + gl < dm) acc[q[r]] += kv[p][r];
-                }
-            }
-            __syncwarp();
-            load(p, k + PF);
-        }
-    }
-    (void)gmask;
-    for (int i = gl; i < block; i += G) __stcs(values + vb + i, acc[i]);
-}
-
-// ---------------------------------------------------------------------------
-// Deterministic owner-computes gather, persistent streaming form (FEA_DET_SORTED)
-// ---------------------------------------------------------------------------
-// A group of G lanes owns a contiguous range of nodes [va, vb); each node's d rows
-// are one contiguous block of values. Incidence lists of consecutive nodes are
-// contiguous, so the group's work is ONE stream of element-matrix row blocks
-// ("chunks") K[e][a*d..a*d+d-1][:], chunk t = adj[t] for t in
-// [adj_ptr[va], adj_ptr[vb]), segmented by node — a CSR segmented reduction. The
-// group keeps PF chunks in flight in registers (R rounds of G doubles each),
-// continuously across node boundaries. Chunk indices and position-map words are
-// staged through a per-group shared-memory ring: loaded into registers one block
-// (kBlk chunks) early and stored when the block before is finished, so no
-// dependent global load ever sits between two chunk loads. Each chunk is folded
-// into the node's shared accumulator in ascending element order (group-local
-// __syncwarp between chunks: a per-slot left fold from the slot's start value,
-// bit-identical to assemble_sequential, assembly.hpp:112-118); at a node boundary
-// the block is written once with coalesced streaming stores. K is read exactly
-// once, values written once, no atomics.
-constexpr int kPosW = 8;  // max position-map words staged per lane per block
-template <int G>
-constexpr int blk_of() { return G < 16 ? 16 : G; }  // chunks per staging block (>= G)
-
-template <int R>
-constexpr int gather_min_blocks() { return R >= 8 ? FEA_GATHER_MIN_BLOCKS_WIDE : FEA_GATHER_MIN_BLOCKS; }
-
-template <int G, int R, int PF, class PosT, bool DISTINCT>
-__global__ void __launch_bounds__(kWarps * 32, gather_min_blocks<R>())
-    k_gather_stream(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
-             const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
-             const int64_t* __restrict__ nptr, int64_t n_own, int64_t n_groups, int d, int npe,
-             int pstride, int acc_stride, int accumulate, double* __restrict__ values) {
-    extern __shared__ double sacc[];
-    constexpr int GPW = 32 / G;
-    constexpr int kBlk = blk_of<G>();
-    constexpr int EPL = kBlk / G;  // staged chunk indices per lane per block
-    const int m = d * npe;
-    const int dm = d * m;
-    const int lane = threadIdx.x & 31;
-    const int gl = lane % G;
-    const int gw = lane / G;
-    const int warp = threadIdx.x >> 5;
-    const int grp = warp * GPW + gw;
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
-    const int pw_blk = kBlk * pstride * static_cast<int>(sizeof(PosT)) / 4;  // words per block
-    double* acc = sacc + static_cast<int64_t>(grp) * acc_stride;
-    int32_t* ring = reinterpret_cast<int32_t*>(sacc + static_cast<int64_t>(kWarps) * GPW * acc_stride) +
-                    static_cast<int64_t>(grp) * 2 * (kBlk + pw_blk);
-    int32_t* ent_ring = ring;                 // [2][kBlk]
-    uint32_t* pos_ring = reinterpret_cast<uint32_t*>(ring + 2 * kBlk);  // [2][pw_blk] words
-
-    uint32_t tab[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int idx = r * G + gl;
-        const int ki = idx / m;
-        const int j = idx - ki * m;
-        const int b = j / d;
-        tab[r] = idx < dm ? (static_cast<uint32_t>(ki) | (static_cast<uint32_t>(b) << 10) |
-                             (static_cast<uint32_t>(j - b * d) << 20))
-                          : 0u;
-    }
-
-    const int64_t g = (static_cast<int64_t>(blockIdx.x) * kWarps + warp) * GPW + gw;
-    const int64_t va = n_own * g / n_groups;
-    const int64_t vend = n_own * (g + 1) / n_groups;
-    if (va >= vend) return;
-    const int64_t t0 = adj_ptr[va];
-    const int64_t t_end = adj_ptr[vend];
-    const uint32_t* pos_words = reinterpret_cast<const uint32_t*>(posA);
-    const int64_t pw_end = t_end * pstride * static_cast<int64_t>(sizeof(PosT)) / 4;
-
-    int32_t se[EPL];
-    uint32_t sp[kPosW];
-    auto load_block = [&](int64_t blk) {
-        const int64_t tb = t0 + blk * kBlk;
-#pragma unroll
-        for (int i = 0; i < EPL; ++i) {
-            const int64_t t = tb + i * G + gl;
-            se[i] = t < t_end ? adj[t] : 0;
-        }
-        const int64_t wb = tb * pstride * static_cast<int64_t>(sizeof(PosT)) / 4;
-#pragma unroll
-        for (int i = 0; i < kPosW; ++i) {
-            const int q = i * G + gl;
-            if (q < pw_blk && wb + q < pw_end) sp[i] = pos_words[wb + q];
-        }
-    };
-    auto store_block = [&](int64_t blk) {
-        const int slot = static_cast<int>(blk & 1);
-#pragma unroll
-        for (int i = 0; i < EPL; ++i) ent_ring[slot * kBlk + i * G + gl] = se[i];
-#pragma unroll
-        for (int i = 0; i < kPosW; ++i) {
-            const int q = i * G + gl;
-            if (q < pw_blk) pos_ring[slot * pw_blk + q] = sp[i];
-        }
-    };
-    load_block(0);
-    store_block(0);
-    load_block(1);
-    store_block(1);
-    load_block(2);
-    __syncwarp(gmask);
-
-    int64_t v = va;
-    int64_t seg_end = adj_ptr[v + 1];
-    int64_t c0 = nptr[v];
-    int rowlen = static_cast<int>(d * (nptr[v + 1] - c0));
-    int block = d * rowlen;
-    int64_t vbase = static_cast<int64_t>(d) * d * c0;
-    for (int i = gl; i < block; i += G) acc[i] = accumulate ? values[vbase + i] : 0.0;
-    __syncwarp(gmask);
-
-    double kv[PF][R];
-    auto issue = [&](int p, int64_t t) {
-        if (t < t_end) {
-            const int32_t e = ent_ring[(t - t0) & (2 * kBlk - 1)];
-            const double* src = K + static_cast<int64_t>(e) * dm;
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-                if (r * G + gl < dm) kv[p][r] = ld_stream(src + r * G + gl);
-        }
-    };
-#pragma unroll
-    for (int p = 0; p < PF; ++p) issue(p, t0 + p);
-
-    const PosT* pos_ring_t = reinterpret_cast<const PosT*>(pos_ring);
-    for (int64_t tt = t0; tt < t_end; tt += PF) {
-#pragma unroll
-        for (int p = 0; p < PF; ++p) {
-            const int64_t t = tt + p;
-            if (t < t_end) {
-                while (t >= seg_end) {  // node boundary: write the finished block(s)
-                    for (int i = gl; i < block; i += G) __stcs(values + vbase + i, acc[i]);
-                    ++v;
-                    seg_end = adj_ptr[v + 1];
-                    c0 = nptr[v];
-                    rowlen = static_cast<int>(d * (nptr[v + 1] - c0));
-                    block = d * rowlen;
-                    vbase = static_cast<int64_t>(d) * d * c0;
-                    __syncwarp(gmask);
-                    for (int i = gl; i < block; i += G) acc[i] = accumulate ? values[vbase + i] : 0.0;
-                    __syncwarp(gmask);
-                }
-                const int64_t rel = t - t0;
-                if ((rel & (kBlk - 1)) == 0 && rel > 0) {  // staging block boundary
-                    const int64_t blk = rel / kBlk;
-                    store_block(blk + 1);  // into the slot of block blk-1 (finished)
-                    load_block(blk + 2);
-                    __syncwarp(gmask);
-                }
-                const PosT* pk = pos_ring_t + (rel & (2 * kBlk - 1)) * pstride;
-                int q[R];
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const uint32_t tb = tab[r];
-                    q[r] = static_cast<int>(tb & 1023u) * rowlen +
-                           static_cast<int>(pk[(tb >> 10) & 1023u]) * d + static_cast<int>(tb >> 20);
-                    FEA_DCHECK(r * G + gl >= dm || (q[r] >= 0 && q[r] < block));
-                }
-                if (DISTINCT) {  // slots of one chunk are distinct: loads, adds, then stores
-                    double a[R];
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (r * G + gl < dm) a[r] = acc[q[r]];
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (r * G + gl < dm) acc[q[r]] = a[r] + kv[p][r];
-                } else {
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (r * G + gl < dm) acc[q[r]] += kv[p][r];
-                }
-                __syncwarp(gmask);
-                issue(p, t + PF);
-            }
-        }
-    }
-    for (;;) {  // the last node and any trailing empty nodes of the range
-        for (int i = gl; i < block; i += G) __stcs(values + vbase + i, acc[i]);
-        if (++v >= vend) break;
-        c0 = nptr[v];
-        rowlen = static_cast<int>(d * (nptr[v + 1] - c0));
-        block = d * rowlen;
-        vbase = static_cast<int64_t>(d) * d * c0;
-        __syncwarp(gmask);
-        for (int i = gl; i < block; i += G) acc[i] = accumulate ? values[vbase + i] : 0.0;
-        __syncwarp(gmask);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Deterministic gather, lane = column node (FEA_DET_SORTED; G >= npe, D = d compile-time)
-// ---------------------------------------------------------------------------
-// The d x d sub-block K[e][a*d+ki][b*d+kj] of an incident row block lands in the d x d block
-// of the node's values at column position pos(b): slot = ki*rowlen + pos(b)*d + kj. With lane
-// = column node b and the D*D rounds = (ki, kj) unrolled at compile time, each lane does ONE
-// position lookup per row block and every slot is a compile-time offset plus one add — the
-// per-entry decode of k_gather_node disappears. The strided K loads (lane b reads d
-// consecutive doubles of each of the d rows) go through L1 (ld.global.nc), which coalesces
-// them back into whole sectors; DRAM traffic is unchanged. Fold order per slot as in
-// k_gather_node: ascending element id, bit-identical to assemble_sequential.
-#ifndef FEA_CN_MINB
-#define FEA_CN_MINB 6
-#endif
-template <int G, int D, int PF, class PosT, bool DISTINCT, bool GEN>
-__global__ void __launch_bounds__(kWarps * 32, FEA_CN_MINB)
-    k_gather_cn(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
-                const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
-                const int64_t* __restrict__ nptr, const int32_t* __restrict__ order, int64_t n_own,
-                int npe, int pstride, int acc_stride, int pos_stride, int accumulate, GenK gen,
-                double* __restrict__ values) {
-    extern __shared__ double sacc[];
-    constexpr int GPW = 32 / G;
-    constexpr int R = D * D;
-    const int m = D * npe;
-    const int dm = D * m;
-    const int lane = threadIdx.x & 31;
-    const int gl = lane % G;
-    const int gw = lane / G;
-    const int warp = threadIdx.x >> 5;
-    const int grp = warp * GPW + gw;
-    const bool col_ok = gl < npe;
-    double* acc = sacc + static_cast<int64_t>(grp) * acc_stride;
-    PosT* spos = reinterpret_cast<PosT*>(sacc + static_cast<int64_t>(kWarps) * GPW * acc_stride) +
-                 static_cast<int64_t>(grp) * pos_stride;
-
-    const int64_t vi = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * GPW + gw;
-    const int64_t v = (order != nullptr && vi < n_own) ? order[vi] : vi;
-    int64_t b0 = 0, vb = 0;
-    int n = 0, rowlen = 0, block = 0;
-    if (vi < n_own) {
-        b0 = adj_ptr[v];
-        n = static_cast<int>(adj_ptr[v + 1] - b0);
-        const int64_t c0 = nptr[v];
-        rowlen = static_cast<int>(D * (nptr[v + 1] - c0));
-        block = D * rowlen;
-        vb = static_cast<int64_t>(D) * D * c0;
-    }
-    const int32_t my_ent = gl < n ? adj[b0 + gl] : 0;
-    for (int q = gl; q < n * npe; q += G) {
-        const int k = q / npe;
-        spos[q] = posA[(b0 + k) * pstride + (q - k * npe)];
-    }
-    for (int i = gl; i < block; i += G) acc[i] = accumulate ? values[vb + i] : 0.0;
-    const int n_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
-    __syncwarp();
-
-    double kv[PF][R];
-    auto load = [&](int p, int k) {
-        const int32_t e0 = __shfl_sync(0xffffffffu, my_ent, (gw * G + (k & (G - 1))) & 31);
-        const int32_t entry = n <= G ? e0 : (k < n ? adj[b0 + k] : 0);
-        if (k < n && col_ok) {
-            if (GEN) {  // fused supplier: generate the d x d sub-block in registers
-                const int64_t krow = entry / npe;
-                const int a = static_cast<int>(entry - krow * npe);
-                const uint64_t he = kgen_elem(gen.seed, gen.ids ? gen.ids[krow] : krow);
-#pragma unroll
-                for (int ki = 0; ki < D; ++ki)
-#pragma unroll
-                    for (int kj = 0; kj < D; ++kj) kv[p][ki * D + kj] = kgen_entry(he, a * D + ki, gl * D + kj);
-            } else {
-                const double* src = K + static_cast<int64_t>(entry) * dm + gl * D;
-#pragma unroll
-                for (int ki = 0; ki < D; ++ki)
-#pragma unroll
-                    for (int kj = 0; kj < D; ++kj) kv[p][ki * D + kj] = __ldg(src + ki * m + kj);
-            }
-        }
-    };
-#pragma unroll
-    for (int p = 0; p < PF; ++p) load(p, p);
-
-    for (int k0 = 0; k0 < n_max; k0 += PF) {
-#pragma unroll
-        for (int p = 0; p < PF; ++p) {
-            const int k = k0 + p;
-            if (k < n && col_ok) {
-                const int base = static_cast<int>(spos[k * npe + gl]) * D;
-                FEA_DCHECK(base + (D - 1) * rowlen + D - 1 < block);
-                if (DISTINCT) {
-                    double a[R];
-#pragma unroll
-                    for (int ki = 0; ki < D; ++ki)
-#pragma unroll
-                        for (int kj = 0; kj < D; ++kj) a[ki * D + kj] = acc[ki * rowlen + base + kj];
-#pragma unroll
-                    for (int ki = 0; ki < D; ++ki)
-#pragma unroll
-                        for (int kj = 0; kj < D; ++kj)
-                            acc[ki * rowlen + base + kj] = a[ki * D + kj] + kv[p][ki * D + kj];
-                } else {
-#pragma unroll
-                    for (int ki = 0; ki < D; ++ki)
-#pragma unroll
-                        for (int kj = 0; kj < D; ++kj) acc[ki * rowlen + base + kj] += kv[p][ki * D + kj];
-                }
-            }
-            __syncwarp();
-            load(p, k + PF);
-        }
-    }
-    for (int i = gl; i < block; i += G) __stcs(values + vb + i, acc[i]);
-}
-
-// ---------------------------------------------------------------------------
-// Element-owner scatter: atomics (FEA_ATOMIC) or plain adds within a colour
-// ---------------------------------------------------------------------------
-// tab[idx] = a | ki<<8 | b<<16 | kj<<24 for idx = i*m + j, i = a*d+ki, j = b*d+kj.
-template <int G, class PosT, bool ATOMIC>
-__global__ void __launch_bounds__(kWarps * 32)
-    k_scatter(const double* __restrict__ K, const int32_t* __restrict__ list, int64_t n_list,
-              const int32_t* __restrict__ elem_krow, const int32_t* __restrict__ conn_k,
-              const PosT* __restrict__ posE, const int64_t* __restrict__ nptr, int64_t node_begin,
-              int64_t n_own, int d, int npe, double* __restrict__ values) {
-    extern __shared__ unsigned char smem[];
-    constexpr int GPW = 32 / G;
-    const int m = d * npe;
-    const int mm = m * m;
-    uint32_t* tab = reinterpret_cast<uint32_t*>(smem);
-    const int tab_words = (mm + 1) & ~1;
-    int64_t* rb_all = reinterpret_cast<int64_t*>(tab + tab_words);
-    int32_t* rl_all = reinterpret_cast<int32_t*>(rb_all + kWarps * GPW * npe);
-    for (int idx = threadIdx.x; idx < mm; idx += blockDim.x) {
-        const int i = idx / m, j = idx - (idx / m) * m;
-        const int a = i / d, b = j / d;
-        tab[idx] = static_cast<uint32_t>(a) | (static_cast<uint32_t>(i - a * d) << 8) |
-                   (static_cast<uint32_t>(b) << 16) | (static_cast<uint32_t>(j - b * d) << 24);
-    }
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int gl = lane % G;
-    const int gw = lane / G;
-    const int warp = threadIdx.x >> 5;
-    int64_t* rb = rb_all + (warp * GPW + gw) * npe;
-    int32_t* rl = rl_all + (warp * GPW + gw) * npe;
-    const int64_t stride_groups = ((int64_t)gridDim.x * blockDim.x >> 5) * GPW;
-    for (int64_t gi = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * GPW + gw;
-         gi - gw < n_list; gi += stride_groups) {
-        const bool active = gi < n_list;
-        int32_t le = 0, kr = 0;
-        if (active) {
-            le = list[gi];
-            kr = elem_krow[le];
-            for (int a = gl; a < npe; a += G) {
-                const int64_t v = conn_k[static_cast<int64_t>(kr) * npe + a] - node_begin;
-                const bool own = v >= 0 && v < n_own;
-                rb[a] = own ? static_cast<int64_t>(d) * d * nptr[v] : -1;
-                rl[a] = own ? static_cast<int32_t>(d * (nptr[v + 1] - nptr[v])) : 0;
-            }
-        }
-        __syncwarp();
-        if (active) {
-            const double* src = K + static_cast<int64_t>(kr) * mm;
-            const PosT* pe = posE + static_cast<int64_t>(le) * npe * npe;
-#pragma unroll 4
-            for (int idx = gl; idx < mm; idx += G) {
-                const uint32_t t = tab[idx];
-                const int a = t & 0xff, ki = (t >> 8) & 0xff, b = (t >> 16) & 0xff, kj = t >> 24;
-                const int64_t base = rb[a];
-                const double x = ld_stream(src + idx);
-                if (base >= 0) {
-                    const int64_t s = base + static_cast<int64_t>(ki) * rl[a] +
-                                      static_cast<int64_t>(pe[a * npe + b]) * d + kj;
-                    FEA_DCHECK(s >= base && s < base + static_cast<int64_t>(d) * rl[a]);
-                    if (ATOMIC) atomicAdd(values + s, x);
-                    else values[s] += x;
-                }
-            }
-        }
-        __syncwarp();
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Element-order maps for the element-owner routes (built lazily)
-// ---------------------------------------------------------------------------
-template <class PosT>
-__global__ void k_pos_elem(const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
-                           int64_t n_adj, int npe, int pstride, const int32_t* __restrict__ k2l,
-                           PosT* __restrict__ posE) {
-    const int64_t total = n_adj * npe;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t k = t / npe;
-        const int b = static_cast<int>(t - k * npe);
-        const int32_t entry = adj[k];
-        const int32_t kr = entry / npe;
-        const int a = entry - kr * npe;
-        const int64_t le = k2l ? k2l[kr] : kr;
-        posE[(le * npe + a) * npe + b] = posA[k * pstride + b];
-    }
-}
-
-__global__ void k_k2l(const int32_t* __restrict__ elem_krow, int64_t E, int32_t* __restrict__ k2l) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
-         i += (int64_t)gridDim.x * blockDim.x)
-        k2l[elem_krow[i]] = static_cast<int32_t>(i);
-}
-
-// consecutive-element node sharing (locality test) and min-node sort keys
-__global__ void k_locality(const int32_t* __restrict__ conn_k, const int32_t* __restrict__ elem_krow,
-                           int64_t E, int npe, unsigned long long* shared_pairs,
-                           uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t* c = conn_k + static_cast<int64_t>(elem_krow[i]) * npe;
-        uint32_t mn = 0xffffffffu;
-        for (int a = 0; a < npe; ++a) mn = min(mn, static_cast<uint32_t>(c[a]));
-        keys[i] = mn;
-        vals[i] = static_cast<int32_t>(i);
-        if (i > 0) {
-            const int32_t* q = conn_k + static_cast<int64_t>(elem_krow[i - 1]) * npe;
-            bool sh = false;
-            for (int a = 0; a < npe && !sh; ++a)
-                for (int b = 0; b < npe; ++b)
-                    if (c[a] == q[b]) { sh = true; break; }
-            if (sh) atomicAdd(shared_pairs, 1ull);
-        }
-    }
-}
-
-__global__ void k_iota32(int32_t* x, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        x[i] = static_cast<int32_t>(i);
-}
-
-__global__ void k_fill_k(double* __restrict__ K, int64_t n, int m, uint64_t seed,
-                         const int64_t* __restrict__ ids) {
-    const int64_t mm = static_cast<int64_t>(m) * m;
-    const int64_t total = n * mm;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t e = t / mm;
-        const int rem = static_cast<int>(t - e * mm);
-        const int i = rem / m, j = rem - (rem / m) * m;
-        K[t] = kval(seed, ids ? ids[e] : e, i, j);
-    }
-}
-
-template <class F>
-void cub_call(F&& f) {
-    size_t tb = 0;
-    FEA_CK(f(nullptr, tb));
-    DevBuf t;
-    t.alloc(tb);
-    FEA_CK(f(t.p, tb));
-}
-
-// --- launch helpers --------------------------------------------------------
-
-GenK gen_of(const fea_plan* p) {
-    GenK g{};
-    g.on = p->gen_on ? 1 : 0;
-    g.seed = p->gen_seed;
-    g.ids = (p->k_compact && p->partitioned) ? p->elem_id.as<int64_t>() : nullptr;
-    return g;
-}
-
-template <int G, int R, int PF, class PosT>
-void run_gather_stream(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
-                       cudaStream_t s) {
-    constexpr int GPW = 32 / G;
-    const int acc_stride = p->d * p->d * p->max_cnt + 1;  // +1 staggers groups across banks
-    constexpr int kBlk = blk_of<G>();
-    const int pw_blk = kBlk * p->pstride * static_cast<int>(sizeof(PosT)) / 4;
-    FEA_REQUIRE((pw_blk + G - 1) / G <= kPosW, FEA_ERR_INVALID,
-                "position map of one element too large for the gather kernel's staging");
-    const size_t smem = static_cast<size_t>(kWarps) * GPW *
-                        (acc_stride * sizeof(double) + 2 * (kBlk + pw_blk) * sizeof(int32_t));
-    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID,
-                "node row block too large for shared-memory accumulation");
-    auto kern = p->dup_nodes ? k_gather_stream<G, R, PF, PosT, false> : k_gather_stream<G, R, PF, PosT, true>;
-    FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0, n_sm = 0;
-    FEA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kWarps * 32, smem));
-    FEA_CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, p->device));
-    if (p->n_own == 0) return;
-    // persistent: one wave of CTAs, each group a contiguous node range (>= 2 nodes per group)
-    int64_t blocks = static_cast<int64_t>(std::max(occ, 1)) * n_sm;
-    blocks = std::min<int64_t>(blocks, (p->n_own + 2 * kWarps * GPW - 1) / (2 * kWarps * GPW));
-    blocks = std::max<int64_t>(blocks, 1);
-    const int64_t n_groups = blocks * kWarps * GPW;
-    kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
-        K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const PosT*>(in.posA), p->nptr.as<int64_t>(),
-        p->n_own, n_groups, p->d, p->npe, p->pstride, acc_stride, accumulate ? 1 : 0, values);
-    FEA_CK(cudaGetLastError());
-    p->last_launches += 1;
-}
-
-template <int G, int R, int PF, class PosT>
-void run_gather_node(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
-                     cudaStream_t s) {
-    constexpr int GPW = 32 / G;
-    const int acc_stride = p->d * p->d * p->max_cnt + 1;  // +1 staggers groups across banks
-    const int pos_stride = static_cast<int>((std::max<int64_t>(p->max_adj, 1) * p->npe + 7) & ~int64_t(7));
-    size_t smem = static_cast<size_t>(kWarps) * GPW *
-                  (acc_stride * sizeof(double) + pos_stride * sizeof(PosT));
-    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID,
-                "node row block too large for shared-memory accumulation");
-    auto kern = p->gen_on ? (p->dup_nodes ? k_gather_node<G, R, PF, PosT, false, true>
-                                          : k_gather_node<G, R, PF, PosT, true, true>)
-                          : (p->dup_nodes ? k_gather_node<G, R, PF, PosT, false, false>
-                                          : k_gather_node<G, R, PF, PosT, true, false>);
-    if (smem > 48 * 1024)
-        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t groups = p->n_own;
-    const int64_t blocks = (groups + kWarps * GPW - 1) / (kWarps * GPW);
-    if (blocks == 0) return;
-    kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
-        K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const PosT*>(in.posA),
-        p->nptr.as<int64_t>(), p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, p->d,
-        p->npe, p->pstride, acc_stride, pos_stride, accumulate ? 1 : 0, p->d * p->m * 8 < 128 ? 1 : 0,
-        gen_of(p), values);
-    FEA_CK(cudaGetLastError());
-    p->last_launches += 1;
-}
-
-// Kernel choice (measured): one lane group per warp (G == 32, large element
-// blocks) streams persistently; smaller blocks run one node per lane group, many warps.
-template <int G, int R, int PF, class PosT>
-void run_gather(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
-                cudaStream_t s) {
-    if (G == 32 && R >= 8 && !p->node_order.p && !p->gen_on) run_gather_stream<G, R, PF, PosT>(p, in, K, values, accumulate, s);
-    else run_gather_node<G, R, PF, PosT>(p, in, K, values, accumulate, s);
-}
-
-#ifndef FEA_CN_PF8
-#define FEA_CN_PF8 2
-#endif
-template <int G, int D, int PF, class PosT>
-void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
-                   cudaStream_t s) {
-    constexpr int GPW = 32 / G;
-    const int acc_stride = p->d * p->d * p->max_cnt + 1;
-    const int pos_stride = static_cast<int>((std::max<int64_t>(p->max_adj, 1) * p->npe + 7) & ~int64_t(7));
-    const size_t smem = static_cast<size_t>(kWarps) * GPW *
-                        (acc_stride * sizeof(double) + pos_stride * sizeof(PosT));
-    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
-    auto kern = p->gen_on ? (p->dup_nodes ? k_gather_cn<G, D, PF, PosT, false, true>
-                                          : k_gather_cn<G, D, PF, PosT, true, true>)
-                          : (p->dup_nodes ? k_gather_cn<G, D, PF, PosT, false, false>
-                                          : k_gather_cn<G, D, PF, PosT, true, false>);
-    if (smem > 48 * 1024)
-        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t blocks = (p->n_own + kWarps * GPW - 1) / (kWarps * GPW);
-    if (blocks == 0) return;
-    kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
-        K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const PosT*>(in.posA), p->nptr.as<int64_t>(),
-        p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, p->npe, p->pstride, acc_stride,
-        pos_stride, accumulate ? 1 : 0, gen_of(p), values);
-    FEA_CK(cudaGetLastError());
-    p->last_launches += 1;
-}
-
-template <class PosT>
-void gather(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
-            cudaStream_t s) {
-    const int dm = p->d * p->m;
-    // lane = column node (d in {2,3,4}, npe <= 32); measured faster than the decode-table
-    // kernels for every such shape
-    if (!p->cn_disabled && p->d >= 2 && p->d <= 4 && p->npe <= 32) {
-        const int G = p->npe <= 4 ? 4 : p->npe <= 8 ? 8 : p->npe <= 16 ? 16 : 32;
-        switch (G * 10 + p->d) {
-            case 42: return run_gather_cn<4, 2, 2, PosT>(p, in, K, values, accumulate, s);
-            case 43: return run_gather_cn<4, 3, 2, PosT>(p, in, K, values, accumulate, s);
-            case 44: return run_gather_cn<4, 4, 2, PosT>(p, in, K, values, accumulate, s);
-            case 82: return run_gather_cn<8, 2, 2, PosT>(p, in, K, values, accumulate, s);
-            case 83: return run_gather_cn<8, 3, FEA_CN_PF8, PosT>(p, in, K, values, accumulate, s);
-            case 84: return run_gather_cn<8, 4, 2, PosT>(p, in, K, values, accumulate, s);
-            case 163: return run_gather_cn<16, 3, 2, PosT>(p, in, K, values, accumulate, s);
-            case 323: return run_gather_cn<32, 3, 2, PosT>(p, in, K, values, accumulate, s);
-            default: break;
-        }
-    }
-    if (dm <= 4) run_gather<4, 1, 8, PosT>(p, in, K, values, accumulate, s);
-    else if (dm <= 8) run_gather<8, 1, 8, PosT>(p, in, K, values, accumulate, s);
-    else if (dm <= 16) run_gather<16, 1, 4, PosT>(p, in, K, values, accumulate, s);
-    else if (dm <= 32) run_gather<32, 1, 4, PosT>(p, in, K, values, accumulate, s);
-#ifndef FEA_HEX8_PF
-#define FEA_HEX8_PF 2
-#endif
-    else if (dm == 72) run_gather<8, 9, FEA_HEX8_PF, PosT>(p, in, K, values, accumulate, s);
-    else if (dm <= 128) run_gather<32, 4, 2, PosT>(p, in, K, values, accumulate, s);
-    else if (dm <= 256) run_gather<32, 8, 2, PosT>(p, in, K, values, accumulate, s);
-    else if (dm <= 512) run_gather<32, 16, 1, PosT>(p, in, K, values, accumulate, s);
-    else throw Error(FEA_ERR_INVALID, "element row block (d*m) larger than 512 entries");
-}
-
-template <int G, class PosT, bool ATOMIC>
-void run_scatter(fea_plan* p, const double* K, const int32_t* list, int64_t n_list, double* values,
-                 cudaStream_t s) {
-    if (n_list == 0) return;
-    constexpr int GPW = 32 / G;
-    const int mm = p->m * p->m;
-    const size_t smem = static_cast<size_t>((mm + 1) & ~1) * 4 +
-                        static_cast<size_t>(kWarps) * GPW * p->npe * (8 + 4);
-    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "element matrix too large for the scatter kernel");
-    auto kern = k_scatter<G, PosT, ATOMIC>;
-    if (smem > 48 * 1024)
-        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t blocks = std::min<int64_t>((n_list + kWarps * GPW - 1) / (kWarps * GPW), 148 * 16);
-    kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
-        K, list, n_list, p->elem_krow.as<int32_t>(), p->conn_k.as<int32_t>(), p->posE.as<PosT>(),
-        p->nptr.as<int64_t>(), p->node_begin, p->n_own, p->d, p->npe, values);
-    FEA_CK(cudaGetLastError());
-    p->last_launches += 1;
-}
-
-template <class PosT, bool ATOMIC>
-void scatter(fea_plan* p, const double* K, const int32_t* list, int64_t n_list, double* values,
-             cudaStream_t s) {
-    const int mm = p->m * p->m;
-    if (mm <= 4) run_scatter<4, PosT, ATOMIC>(p, K, list, n_list, values, s);
-    else if (mm <= 8) run_scatter<8, PosT, ATOMIC>(p, K, list, n_list, values, s);
-    else if (mm <= 16) run_scatter<16, PosT, ATOMIC>(p, K, list, n_list, values, s);
-    else run_scatter<32, PosT, ATOMIC>(p, K, list, n_list, values, s);
-}
-
-}  // namespace
 
 void ensure_element_maps(fea_plan* p, cudaStream_t s) {
     if (p->posE.p && p->order.p) return;
@@ -1017,23 +103,23 @@ void assemble(fea_plan* p, const double* K, int strategy, double* values, uint32
         // the summation order of the per-colour passes of assemble_coloured_vectorized.
         Incidences in{p->adj.as<int32_t>(), p->posA.p};
         if (strategy == FEA_DET_COLOUR) in = Incidences{p->adjC.as<int32_t>(), p->posAC.p};
-        if (p->pos_bytes == 1) gather<uint8_t>(p, in, K, values, !overwrite, s);
-        else gather<uint16_t>(p, in, K, values, !overwrite, s);
+        if (p->pos_bytes == 1) gather_u8(p, in, K, values, !overwrite, s);
+        else gather_u16(p, in, K, values, !overwrite, s);
         return;
     }
     ensure_element_maps(p, s);
     if (overwrite && p->nnz > 0) FEA_CK(cudaMemsetAsync(values, 0, p->nnz * 8, s));
     if (strategy == FEA_ATOMIC) {
-        if (p->pos_bytes == 1) scatter<uint8_t, true>(p, K, p->order.as<int32_t>(), p->E, values, s);
-        else scatter<uint16_t, true>(p, K, p->order.as<int32_t>(), p->E, values, s);
+        if (p->pos_bytes == 1) scatter_u8(p, K, p->order.as<int32_t>(), p->E, values, true, s);
+        else scatter_u16(p, K, p->order.as<int32_t>(), p->E, values, true, s);
         return;
     }
     const int nc = static_cast<int>(p->colour_off.size()) - 1;
     for (int c = 0; c < nc; ++c) {
         const int32_t* list = p->colour_elems.as<int32_t>() + p->colour_off[c];
         const int64_t cnt = p->colour_off[c + 1] - p->colour_off[c];
-        if (p->pos_bytes == 1) scatter<uint8_t, false>(p, K, list, cnt, values, s);
-        else scatter<uint16_t, false>(p, K, list, cnt, values, s);
+        if (p->pos_bytes == 1) scatter_u8(p, K, list, cnt, values, false, s);
+        else scatter_u16(p, K, list, cnt, values, false, s);
     }
 }
 
