@@ -828,7 +828,7 @@ template <int G, int D, int PF, class PosT>
 void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
                    cudaStream_t s) {
     constexpr int GPW = 32 / G;
-    const int acc_stride = p->d * p->d * p->max_cnt + 1;
+    const int acc_stride = p->d * p->d * p->max_cnt + 1;  // +1 staggers groups across banks (swept: 1-2 best)
     const int pos_stride = static_cast<int>((std::max<int64_t>(p->max_adj, 1) * p->npe + 7) & ~int64_t(7));
     const size_t smem = static_cast<size_t>(kWarps) * GPW *
                         (acc_stride * sizeof(double) + pos_stride * sizeof(PosT));
