@@ -8,7 +8,8 @@
 
 Mesh specs: "gen:N" is the reference's structured n-by-n quad mesh (mesh.cpp:62-85); the 3D
 BASELINE meshes are "hex8:N", "tet4:N", "hex27:N", optionally suffixed ":perm-elements" or
-":perm-nodes" (seed 7). MSH files and p > 1 DOF numbering are out of scope.
+":perm-nodes" (seed 7); an ".msh" path is read as ASCII MSH 2.2 (msh.py: quads, tet4, hex8).
+p > 1 hierarchical DOF numbering is out of scope.
 Methods: seq (the deterministic sort-by-slot route, bit-identical to assemble_sequential),
 atomic, colour-vec (bit-identical to assemble_coloured_vectorized under the greedy colouring);
 spin and spin-vec have no GPU counterpart. Exit codes as the reference (fea_main.cpp:34-37):
@@ -34,12 +35,24 @@ class UsageError(Exception):
 
 
 def parse_mesh(spec: str):
-    """-> (label, n, conn, n_nodes)."""
+    """-> (label, n, conn, n_nodes). A path to an ASCII MSH 2.2 file is read with msh.import_msh
+    (quads, or one volume type: tet4 / hex8); warnings go to stderr like the reference."""
+    import os
+    if spec.endswith(".msh") or os.path.isfile(spec):
+        from . import msh
+        try:
+            text = open(spec).read()
+        except OSError as e:
+            raise UsageError(f"cannot read {spec}: {e}") from None
+        conn, nn, _, warnings, _ = msh.import_msh(text, kind="auto")
+        for w in warnings:
+            print(f"warning: {spec}: {w}", file=sys.stderr)
+        return spec, 0, conn, nn
     parts = spec.split(":")
     kind = parts[0]
     if kind not in ("gen", "quad4", "hex8", "tet4", "hex27") or len(parts) < 2:
-        raise UsageError(f"mesh spec '{spec}': expected gen:N or hex8|tet4|hex27:N[:perm-elements|perm-nodes]"
-                         " (MSH files are not supported)")
+        raise UsageError(f"mesh spec '{spec}': expected gen:N, hex8|tet4|hex27:N[:perm-elements|perm-nodes] "
+                         "or an .msh file")
     try:
         n = int(parts[1])
     except ValueError:

@@ -10,7 +10,7 @@ from paper_2012_00585_b200 import cli
 def test_usage_errors_exit_1():
     assert cli.main(["bench", "--methods", "spin"]) == cli.EXIT_USAGE
     assert cli.main(["bench", "--methods", "bogus"]) == cli.EXIT_USAGE
-    assert cli.main(["assemble", "--mesh", "file.msh"]) == cli.EXIT_USAGE
+    assert cli.main(["assemble", "--mesh", "missing.msh"]) == cli.EXIT_USAGE
     assert cli.main(["assemble", "--mesh", "gen:0"]) == cli.EXIT_USAGE
     assert cli.main(["assemble", "--p", "3"]) == cli.EXIT_USAGE
     assert cli.main([]) == cli.EXIT_USAGE
