@@ -153,6 +153,13 @@ FEA_API fea_status fea_plan_copy_elements(const fea_plan* plan, int64_t* elem_id
  * ascending id, = all E for a whole-matrix plan). */
 FEA_API fea_status fea_plan_greedy_colouring(const fea_plan* plan, int32_t* colour_of, int32_t* n_colours);
 
+/* Jones-Plassmann colouring computed on the device (seeded priorities): a valid colouring in
+ * a few kernel rounds instead of the sequential greedy pass; it is NOT the reference's greedy
+ * colouring, so FEA_DET_COLOUR is bit-identical to assemble_coloured_vectorized run with this
+ * same colouring. colour_of[n_elements] (host). */
+FEA_API fea_status fea_plan_jp_colouring(const fea_plan* plan, uint64_t seed, int32_t* colour_of,
+                                         int32_t* n_colours);
+
 /* Install the colouring used by FEA_DET_COLOUR (Colouring::colour_of,
  * colouring.hpp:35-39; host or device array over the plan's kept elements).
  * Validated like find_colour_conflict (colouring.cpp:91-119): two same-colour

@@ -50,6 +50,7 @@ SIGNATURES = {
     "fea_plan_copy_elements": (c_int, [c_void_p, c_void_p]),
     "fea_plan_greedy_colouring": (c_int, [c_void_p, c_void_p, _P32]),
     "fea_plan_set_colouring": (c_int, [c_void_p, c_void_p]),
+    "fea_plan_jp_colouring": (c_int, [c_void_p, c_uint64, c_void_p, _P32]),
     "fea_assemble": (c_int, [c_void_p, c_void_p, c_int32, c_void_p, c_uint32, c_void_p]),
     "fea_assemble_host": (c_int, [c_void_p, c_void_p, c_int32, c_void_p, c_uint32, c_void_p]),
     "fea_assemble_host_batch": (c_int, [c_void_p, POINTER(c_void_p), c_int32, POINTER(c_void_p),

@@ -148,6 +148,13 @@ class Plan:
         _check(self._lib.fea_plan_greedy_colouring(self._h, _ptr(col), byref(nc)))
         return col[: self.n_elements], nc.value
 
+    def jp_colouring(self, seed: int = 1):
+        """Jones-Plassmann colouring on the device (valid; differs from the greedy one)."""
+        col = np.empty(max(self.n_elements, 1), np.int32)
+        nc = c_int32()
+        _check(self._lib.fea_plan_jp_colouring(self._h, ctypes.c_uint64(seed), _ptr(col), byref(nc)))
+        return col[: self.n_elements], nc.value
+
     def set_colouring(self, colour_of) -> None:
         col = np.ascontiguousarray(colour_of, dtype=np.int32)
         _check(self._lib.fea_plan_set_colouring(self._h, _ptr(col)))

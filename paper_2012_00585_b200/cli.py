@@ -241,7 +241,7 @@ def cmd_colour(a) -> int:
     from .assembly import Plan
     label, n, conn, nn = parse_mesh(a.mesh)
     plan = Plan(M.element_dofs(conn, 1), nn)
-    col, nc = plan.greedy_colouring()
+    col, nc = plan.jp_colouring(seed=a.seed) if a.jp else plan.greedy_colouring()
     print(f"mesh {label}: {len(col)} elements, {nc} colours")
     for c in range(nc):  # colour_distribution, colouring.cpp:77-89
         print(f"  colour {c}: {np.count_nonzero(col == c) / max(len(col), 1):.4f}")
@@ -285,6 +285,8 @@ def build_parser() -> argparse.ArgumentParser:
     s.add_argument("--mesh", default="gen:8")
     s.add_argument("--p", type=int, default=1)
     s.add_argument("--out", default=None, help="CSV dump path (element,colour)")
+    s.add_argument("--jp", action="store_true", help="Jones-Plassmann colouring on the GPU instead of greedy")
+    s.add_argument("--seed", type=int, default=1)
     return ap
 
 

@@ -550,6 +550,60 @@ __global__ void k_node_share(const int64_t* __restrict__ adj_ptr, const int32_t*
     }
 }
 
+// Jones-Plassmann colouring (GPU colouring): every round, each
+// uncoloured element whose seeded priority beats all uncoloured elements sharing an (owned)
+// node takes the smallest colour no coloured neighbour uses. Two neighbours are never local
+// maxima in the same round, so colours read from neighbours are stable within a round.
+__global__ void k_jp_prio(const int64_t* __restrict__ elem_id, int64_t E, uint64_t seed,
+                          uint64_t* __restrict__ prio, int32_t* __restrict__ colour) {
+    for (int64_t le = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; le < E;
+         le += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t z = seed + static_cast<uint64_t>(elem_id[le]) + 0x9e3779b97f4a7c15ULL;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        z ^= z >> 31;
+        prio[le] = (z & ~0xffffffffULL) | static_cast<uint32_t>(le);  // ties broken by index
+        colour[le] = -1;
+    }
+}
+
+__global__ void k_jp_round(const int32_t* __restrict__ conn_k, const int32_t* __restrict__ elem_krow,
+                           const int32_t* __restrict__ k2l, int64_t E, int npe, int64_t node_begin,
+                           int64_t node_end, const int64_t* __restrict__ adj_ptr,
+                           const int32_t* __restrict__ adj, const uint64_t* __restrict__ prio,
+                           int32_t* __restrict__ colour, unsigned long long* __restrict__ remaining) {
+    for (int64_t le = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; le < E;
+         le += (int64_t)gridDim.x * blockDim.x) {
+        if (colour[le] >= 0) continue;
+        const uint64_t mine = prio[le];
+        const int32_t* c = conn_k + static_cast<int64_t>(elem_krow[le]) * npe;
+        uint64_t used[2] = {0, 0};
+        bool local_max = true;
+        for (int a = 0; a < npe && local_max; ++a) {
+            const int64_t v = c[a];
+            if (v < node_begin || v >= node_end) continue;
+            const int64_t lv = v - node_begin;
+            for (int64_t k = adj_ptr[lv]; k < adj_ptr[lv + 1]; ++k) {
+                const int32_t kr = adj[k] / npe;
+                const int64_t o = k2l ? k2l[kr] : kr;
+                if (o == le) continue;
+                const int32_t oc = colour[o];
+                if (oc < 0) {
+                    if (prio[o] > mine) { local_max = false; break; }
+                } else if (oc < 128) {
+                    used[oc >> 6] |= 1ull << (oc & 63);
+                }
+            }
+        }
+        if (!local_max) {
+            atomicAdd(remaining, 1ull);
+            continue;
+        }
+        const int c0 = __ffsll(static_cast<long long>(~used[0]));
+        colour[le] = c0 ? c0 - 1 : 64 + __ffsll(static_cast<long long>(~used[1])) - 1;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Host orchestration
 // ---------------------------------------------------------------------------
@@ -1294,6 +1348,8 @@ fea_status fea_plan_set_colouring(fea_plan* p, const int32_t* colour_of) {
                 const int32_t e = by_colour[i];
                 for (int a = 0; a < npe; ++a) {
                     const int32_t v = conn[static_cast<int64_t>(e) * npe + a];
+                    // only owned rows are assembled: sharing a node outside them is no conflict
+                    if (v < p->node_begin || v >= p->node_end) continue;
                     if (owner[v] >= 0 && owner[v] != e)
                         throw Error(FEA_ERR_INVALID_COLOURING,
                                     "invalid colouring: elements " + std::to_string(owner[v]) +
@@ -1304,8 +1360,10 @@ fea_status fea_plan_set_colouring(fea_plan* p, const int32_t* colour_of) {
                 }
             }
             for (int64_t i = off[c]; i < off[c + 1]; ++i)
-                for (int a = 0; a < npe; ++a)
-                    owner[conn[static_cast<int64_t>(by_colour[i]) * npe + a]] = -1;
+                for (int a = 0; a < npe; ++a) {
+                    const int32_t v = conn[static_cast<int64_t>(by_colour[i]) * npe + a];
+                    if (v >= p->node_begin && v < p->node_end) owner[v] = -1;
+                }
         }
         p->colour_elems.alloc(by_colour.size() * 4);
         if (!by_colour.empty())
@@ -1314,6 +1372,59 @@ fea_status fea_plan_set_colouring(fea_plan* p, const int32_t* colour_of) {
         p->colour_off = off;
         build_colour_incidences(p, col, st.s);
         p->has_colouring = true;
+    });
+}
+
+// Jones-Plassmann colouring on the device (a valid colouring, not the greedy one; the colour
+// routes stay bit-identical to assemble_coloured_vectorized under whichever colouring is set).
+fea_status fea_plan_jp_colouring(const fea_plan* p, uint64_t seed, int32_t* colour_of, int32_t* n_colours) {
+    return guarded([&] {
+        FEA_REQUIRE(p && (p->E == 0 || colour_of), FEA_ERR_INVALID, "NULL argument");
+        DeviceScope ds(p->device);
+        Stream st;
+        cudaStream_t s = st.s;
+        if (p->E == 0) {
+            if (n_colours) *n_colours = 0;
+            return;
+        }
+        DevBuf prio, col, rem, k2l;
+        prio.alloc(p->E * 8);
+        col.alloc(p->E * 4);
+        rem.alloc(8);
+        const int32_t* k2l_ptr = nullptr;
+        if (p->partitioned && !p->k_compact) {  // adjacency holds global element ids
+            k2l.alloc(p->E_in * 4);
+            FEA_CK(cudaMemsetAsync(k2l.p, 0xff, k2l.bytes, s));
+            std::vector<int32_t> kr(static_cast<size_t>(p->E)), inv(static_cast<size_t>(p->E_in), -1);
+            FEA_CK(cudaMemcpy(kr.data(), p->elem_krow.p, kr.size() * 4, cudaMemcpyDeviceToHost));
+            for (int64_t le = 0; le < p->E; ++le) inv[kr[le]] = static_cast<int32_t>(le);
+            FEA_CK(cudaMemcpyAsync(k2l.p, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice, s));
+            k2l_ptr = k2l.as<int32_t>();
+        }
+        k_jp_prio<<<grid_for(p->E, 256), 256, 0, s>>>(p->elem_id.as<int64_t>(), p->E, seed,
+                                                      prio.as<uint64_t>(), col.as<int32_t>());
+        FEA_CK(cudaGetLastError());
+        for (int round = 0; round < 100000; ++round) {
+            FEA_CK(cudaMemsetAsync(rem.p, 0, 8, s));
+            k_jp_round<<<grid_for(p->E, 256), 256, 0, s>>>(
+                p->conn_k.as<int32_t>(), p->elem_krow.as<int32_t>(), k2l_ptr, p->E, p->npe, p->node_begin,
+                p->node_end, p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), prio.as<uint64_t>(),
+                col.as<int32_t>(), rem.as<unsigned long long>());
+            FEA_CK(cudaGetLastError());
+            unsigned long long h = 0;
+            FEA_CK(cudaMemcpyAsync(&h, rem.p, 8, cudaMemcpyDeviceToHost, s));
+            FEA_CK(cudaStreamSynchronize(s));
+            if (h == 0) break;
+        }
+        std::vector<int32_t> hc(static_cast<size_t>(p->E));
+        FEA_CK(cudaMemcpy(hc.data(), col.p, hc.size() * 4, cudaMemcpyDeviceToHost));
+        int nc = 0;
+        for (const int32_t c : hc) {
+            FEA_REQUIRE(c >= 0 && c < 128, FEA_ERR_INVALID, "Jones-Plassmann colouring needs more than 128 colours");
+            nc = std::max(nc, c + 1);
+        }
+        std::memcpy(colour_of, hc.data(), hc.size() * 4);
+        if (n_colours) *n_colours = nc;
     });
 }
 

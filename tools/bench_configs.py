@@ -73,6 +73,10 @@ def run_config(cfg, runs, use_oracle):
     col, nc = plan.greedy_colouring()
     plan.set_colouring(col)
     col_s = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, nc_jp = plan.jp_colouring(seed=1)
+    jp_ms = (time.perf_counter() - t0) * 1e3
     K = fea.fill_seeded_k(E, m, M.SEED_K)
     values = torch.zeros(plan.nnz, dtype=torch.float64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -80,7 +84,8 @@ def run_config(cfg, runs, use_oracle):
     min_bytes = 8 * entries + 8 * plan.nnz + 4 * E * npe
     out = {"config": cfg, "name": c["name"], "elements": E, "m": m, "rows": plan.n_rows, "nnz": plan.nnz,
            "crac_runs": plan.n_runs, "n_colours": nc, "symbolic_ms": round(sym_ms, 2),
-           "colouring_host_s": round(col_s, 3), "meshgen_s": round(gen_s, 2),
+           "colouring_host_s": round(col_s, 3), "jp_colouring_gpu_ms": round(jp_ms, 2), "jp_colours": nc_jp,
+           "meshgen_s": round(gen_s, 2),
            "min_bytes": min_bytes, "plan_metadata_bytes": plan.metadata_bytes, "strategies": {}}
     for s in ("sorted", "atomic", "colour", "colour_passes"):
         avg, mn, launches = time_strategy(plan, K, values, s, runs, flush)
