@@ -66,3 +66,69 @@ def gather_row_blocks(values_local, root: int = 0, group=None):
     if rank != root:
         return None
     return torch.cat([o[:s] for o, s in zip(out, sizes)])
+
+
+def _gather_1d(t, root, group):
+    """Gather a 1-D tensor of any length from every rank to `root` (rank order)."""
+    return gather_row_blocks(t, root=root, group=group)
+
+
+def gather_csr_blocks(row_ptr, cols, values, root: int = 0, group=None):
+    """Rebuild the global CSR matrix on `root` from every rank's owned row block
+    (row_ptr rebased to 0 per block, global cols). Returns (row_ptr, cols, values) on root."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    rp = _gather_1d(row_ptr[1:].contiguous(), root, group)  # drop each block's leading 0
+    cs = _gather_1d(cols, root, group)
+    vs = _gather_1d(values, root, group)
+    counts = torch.tensor([row_ptr.numel() - 1, values.numel()], dtype=torch.int64, device=row_ptr.device)
+    world = dist.get_world_size(group)
+    allc = [torch.zeros_like(counts) for _ in range(world)]
+    dist.all_gather(allc, counts, group=group)
+    if rank != root:
+        return None
+    out = [torch.zeros(1, dtype=row_ptr.dtype, device=row_ptr.device)]
+    pos, base = 0, 0
+    for c in allc:
+        nr, nz = int(c[0]), int(c[1])
+        out.append(rp[pos:pos + nr] + base)
+        pos += nr
+        base += nz
+    return torch.cat(out), cs, vs
+
+
+def gather_crac_blocks(crac_ptr, col_align, root: int = 0, group=None):
+    """Rebuild the global CRAC arrays on `root`: each block's row_ptr (col_align entry units) and
+    its (col_start, values_pos) pairs are rebased by the blocks before it; one final (0, nnz)
+    pair closes the result (formats.cpp:36-39)."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    nr = crac_ptr.numel() - 1
+    pairs = col_align[:-2].contiguous()  # drop the block's final pair
+    nnz = col_align[-1:].clone()
+    meta = torch.tensor([nr, pairs.numel(), int(nnz.item())], dtype=torch.int64, device=crac_ptr.device)
+    allm = [torch.zeros_like(meta) for _ in range(world)]
+    dist.all_gather(allm, meta, group=group)
+    rp = _gather_1d(crac_ptr[1:].contiguous(), root, group)
+    pa = _gather_1d(pairs, root, group)
+    if rank != root:
+        return None
+    ptr_out = [torch.zeros(1, dtype=crac_ptr.dtype, device=crac_ptr.device)]
+    pair_out = []
+    rpos = ppos = 0
+    abase = vbase = 0
+    for m in allm:
+        nrb, npb, nzb = int(m[0]), int(m[1]), int(m[2])
+        ptr_out.append(rp[rpos:rpos + nrb] + abase)
+        blk = pa[ppos:ppos + npb].clone()
+        blk[1::2] += vbase
+        pair_out.append(blk)
+        rpos += nrb
+        ppos += npb
+        abase += npb
+        vbase += nzb
+    pair_out.append(torch.tensor([0, vbase], dtype=col_align.dtype, device=col_align.device))
+    return torch.cat(ptr_out), torch.cat(pair_out)

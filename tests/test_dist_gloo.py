@@ -43,10 +43,24 @@ def _worker(rank, world, port, q):
         full_local = P.assemble_sequential(ed[kept], K[kept])
         block = full_local[rp[lo * d]:rp[hi * d]]
         got = dist.gather_row_blocks(torch.from_numpy(block), root=0)
+        # the owned block's CSR / CRAC arrays (rows rebased, global columns), as the plan returns them
+        brp = rp[lo * d:hi * d + 1] - rp[lo * d]
+        _, cs_all = P.arrays()
+        bcs = cs_all[rp[lo * d]:rp[hi * d]]
+        Pb = oracle.Pattern.from_arrays(brp, bcs)
+        bcp, bca = Pb.crac()
+        full = dist.gather_csr_blocks(torch.from_numpy(brp), torch.from_numpy(bcs), torch.from_numpy(block))
+        crac = dist.gather_crac_blocks(torch.from_numpy(bcp), torch.from_numpy(bca))
         if rank == 0:
             Pf = oracle.Pattern.build(conn, nn, d)
             want = Pf.assemble_sequential(ed, K)
-            q.put(bool(got.numpy().tobytes() == want.tobytes()))
+            frp, fcs = Pf.arrays()
+            fcp, fca = Pf.crac()
+            ok = got.numpy().tobytes() == want.tobytes()
+            ok &= np.array_equal(full[0].numpy(), frp) and np.array_equal(full[1].numpy(), fcs)
+            ok &= full[2].numpy().tobytes() == want.tobytes()
+            ok &= np.array_equal(crac[0].numpy(), fcp) and np.array_equal(crac[1].numpy(), fca)
+            q.put(bool(ok))
     finally:
         tdist.destroy_process_group()
 
