@@ -259,9 +259,9 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
 #pragma unroll
         for (int p = 0; p < PF; ++p) {
             const int k = k0 + p;
+            int q[R];
             if (k < n) {
                 const PosT* pk = spos + k * npe;
-                int q[R];
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const uint32_t t = tab[r];
@@ -269,9 +269,11 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
                            static_cast<int>(pk[(t >> 10) & 1023u]) * d + static_cast<int>(t >> 20);
                     FEA_DCHECK(r * G + gl >= dm || (q[r] >= 0 && q[r] < block));
                 }
-                if (DISTINCT) {
-                    // the slots of one element row block are distinct (no repeated node in
-                    // an element): all loads, then all adds, then all stores
+            }
+            if (DISTINCT) {
+                // the slots of one element row block are distinct (no repeated node in an
+                // element): all loads, then all adds, then all stores
+                if (k < n) {
                     double a[R];
 #pragma unroll
                     for (int r = 0; r < R; ++r)
@@ -279,11 +281,16 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_GATHER_MIN_BLOCKS)
 #pragma unroll
                     for (int r = 0; r < R; ++r)
                         if (r * G + gl < dm) acc[q[r]] = a[r] + kv[p][r];
-                } else {
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (r * G + gl < dm) acc[q[r]] += kv[p][r];
                 }
+            } else {
+                // a repeated node: two entries of the row block share a slot; fold them one
+                // entry at a time in entry order (idx = r*G + lane ascending = column order)
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    for (int l = 0; l < G; ++l) {
+                        if (k < n && gl == l && r * G + gl < dm) acc[q[r]] += kv[p][r];
+                        __syncwarp();
+                    }
             }
             __syncwarp();
             load(p, k + PF);
@@ -461,10 +468,13 @@ __global__ void __launch_bounds__(kWarps * 32, gather_min_blocks<R>())
 #pragma unroll
                     for (int r = 0; r < R; ++r)
                         if (r * G + gl < dm) acc[q[r]] = a[r] + kv[p][r];
-                } else {
+                } else {  // a repeated node: shared slots, folded entry by entry in entry order
 #pragma unroll
                     for (int r = 0; r < R; ++r)
-                        if (r * G + gl < dm) acc[q[r]] += kv[p][r];
+                        for (int l = 0; l < G; ++l) {
+                            if (gl == l && r * G + gl < dm) acc[q[r]] += kv[p][r];
+                            __syncwarp(gmask);
+                        }
                 }
                 __syncwarp(gmask);
                 issue(p, t + PF);
@@ -570,10 +580,22 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_CN_MINB)
 #pragma unroll
         for (int p = 0; p < PF; ++p) {
             const int k = k0 + p;
-            if (k < n && col_ok) {
+            if (!DISTINCT) {
+                // a repeated node: two lanes (columns) share slots; fold lane by lane in column order
+                for (int l = 0; l < G; ++l) {
+                    if (k < n && col_ok && gl == l) {
+                        const int base = static_cast<int>(spos[k * npe + gl]) * D;
+#pragma unroll
+                        for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+                            for (int kj = 0; kj < D; ++kj) acc[ki * rowlen + base + kj] += kv[p][ki * D + kj];
+                    }
+                    __syncwarp();
+                }
+            } else if (k < n && col_ok) {
                 const int base = static_cast<int>(spos[k * npe + gl]) * D;
                 FEA_DCHECK(base + (D - 1) * rowlen + D - 1 < block);
-                if (DISTINCT) {
+                {
                     double a[R];
 #pragma unroll
                     for (int ki = 0; ki < D; ++ki)
@@ -584,11 +606,6 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_CN_MINB)
 #pragma unroll
                         for (int kj = 0; kj < D; ++kj)
                             acc[ki * rowlen + base + kj] = a[ki * D + kj] + kv[p][ki * D + kj];
-                } else {
-#pragma unroll
-                    for (int ki = 0; ki < D; ++ki)
-#pragma unroll
-                        for (int kj = 0; kj < D; ++kj) acc[ki * rowlen + base + kj] += kv[p][ki * D + kj];
                 }
             }
             __syncwarp();
@@ -607,7 +624,7 @@ __global__ void __launch_bounds__(kWarps * 32)
     k_scatter(const double* __restrict__ K, const int32_t* __restrict__ list, int64_t n_list,
               const int32_t* __restrict__ elem_krow, const int32_t* __restrict__ conn_k,
               const PosT* __restrict__ posE, const int64_t* __restrict__ nptr, int64_t node_begin,
-              int64_t n_own, int d, int npe, double* __restrict__ values) {
+              int64_t n_own, int d, int npe, int serial, double* __restrict__ values) {
     extern __shared__ unsigned char smem[];
     constexpr int GPW = 32 / G;
     const int m = d * npe;
@@ -648,8 +665,11 @@ __global__ void __launch_bounds__(kWarps * 32)
         if (active) {
             const double* src = K + static_cast<int64_t>(kr) * mm;
             const PosT* pe = posE + static_cast<int64_t>(le) * npe * npe;
+            // a repeated node (serial): entries sharing a slot must be added in (i, j) order by
+            // one lane (scatter_element, assembly.hpp:77-92); atomics need no order
+            const int step = serial && !ATOMIC ? 1 : G;
 #pragma unroll 4
-            for (int idx = gl; idx < mm; idx += G) {
+            for (int idx = serial && !ATOMIC ? (gl == 0 ? 0 : mm) : gl; idx < mm; idx += step) {
                 const uint32_t t = tab[idx];
                 const int a = t & 0xff, ki = (t >> 8) & 0xff, b = (t >> 16) & 0xff, kj = t >> 24;
                 const int64_t base = rb[a];
@@ -898,7 +918,7 @@ void run_scatter(fea_plan* p, const double* K, const int32_t* list, int64_t n_li
     const int64_t blocks = std::min<int64_t>((n_list + kWarps * GPW - 1) / (kWarps * GPW), 148 * 16);
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
         K, list, n_list, p->elem_krow.as<int32_t>(), p->conn_k.as<int32_t>(), p->posE.as<PosT>(),
-        p->nptr.as<int64_t>(), p->node_begin, p->n_own, p->d, p->npe, values);
+        p->nptr.as<int64_t>(), p->node_begin, p->n_own, p->d, p->npe, p->dup_nodes ? 1 : 0, values);
     FEA_CK(cudaGetLastError());
     p->last_launches += 1;
 }

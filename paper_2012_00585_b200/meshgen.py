@@ -145,3 +145,16 @@ def closed_form_nnz(mesh: str, n: int, d: int) -> int:
         N = n + 1
         return d * d * (N ** 3 + 2 * (3 * (N - 1) * N * N + 3 * (N - 1) ** 2 * N + (N - 1) ** 3))
     raise ValueError(mesh)
+
+
+def collapse_elements(conn, rng, frac: float = 0.3):
+    """Degenerate elements (a local node repeated: a quad collapsed to a triangle, a hex to a
+    wedge) for a random `frac` of the elements. scatter_element adds every (i, j) pair, so a
+    repeated node's slots receive several contributions per element, in (i, j) order
+    (assembly.hpp:77-92)."""
+    conn = np.array(conn, copy=True)
+    npe = conn.shape[1]
+    for e in np.flatnonzero(rng.random(conn.shape[0]) < frac):
+        a, b = rng.choice(npe, size=2, replace=False)
+        conn[e, a] = conn[e, b]
+    return conn

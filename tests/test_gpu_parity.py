@@ -388,3 +388,32 @@ def test_colouring_of_partitioned_plan_checks_owned_rows_only(gpu, orc):
         got = plan.assemble(torch.from_numpy(Kh).cuda(), strategy="colour").cpu().numpy()
         assert got.tobytes() == want[rpk[rb]:rpk[re]].tobytes()
         del full_col, rp
+
+
+DEGENERATE = [("quad4", 5, 1, None), ("quad4", 4, 2, "nodes"), ("hex8", 3, 3, "elements"),
+              ("hex8", 3, 1, None), ("tet4", 3, 1, "nodes"), ("tet4", 2, 3, None), ("hex27", 2, 1, None)]
+
+
+@pytest.mark.parametrize("mesh,n,d,perm", DEGENERATE)
+def test_degenerate_elements_all_strategies(gpu, orc, mesh, n, d, perm):
+    """Elements listing a node twice (collapsed quads / wedges): one element row block then
+    hits the same slot from two columns, folded in column order like scatter_element
+    (assembly.hpp:77-92); sorted / colour / colour passes stay bit-exact."""
+    import torch
+    conn, nn = M.make_mesh(mesh, n, perm)
+    conn = M.collapse_elements(conn, np.random.default_rng(n * 10 + d))
+    ed = M.element_dofs(conn, d)
+    P = orc.Pattern.build(conn, nn, d)
+    Kh = orc.fill_k(3, conn.shape[0], ed.shape[1])
+    want = P.assemble_sequential(ed, Kh)
+    col, _ = orc.greedy_colouring(conn, nn)
+    want_col = P.assemble_coloured(ed, Kh, col)
+    K = torch.from_numpy(Kh).cuda()
+    with gpu.Plan(ed, nn * d, dofs_per_node=d) as plan:
+        assert plan.nnz == P.nnz
+        assert plan.assemble(K, strategy="sorted").cpu().numpy().tobytes() == want.tobytes()
+        assert plan.assemble_seeded(3, strategy="sorted").cpu().numpy().tobytes() == want.tobytes()
+        plan.set_colouring(col)
+        assert plan.assemble(K, strategy="colour").cpu().numpy().tobytes() == want_col.tobytes()
+        assert plan.assemble(K, strategy="colour_passes").cpu().numpy().tobytes() == want_col.tobytes()
+        assert close(plan.assemble(K, strategy="atomic").cpu().numpy(), want)

@@ -281,3 +281,24 @@ def test_seeded_k_exact_and_symmetric(orc):
     assert K.min() >= -1.0 and K.max() < 1.0
     # (h>>11) * 2^-53 * 2 - 1 is exact: every value is a multiple of 2^-52
     assert np.all(np.ldexp(K + 1.0, 52) == np.round(np.ldexp(K + 1.0, 52)))
+
+
+def test_degenerate_elements_match_live_reference(orc, ref_lib):
+    rng = np.random.default_rng(77)
+    for trial, (mesh, n, d) in enumerate([("quad4", 4, 1), ("quad4", 3, 2), ("hex8", 2, 3),
+                                           ("tet4", 2, 1), ("hex8", 2, 1)]):
+        conn, nn = M.make_mesh(mesh, n, "nodes" if trial % 2 else None, seed=trial)
+        conn = M.collapse_elements(conn, rng)
+        R = ref_lib.RefProblem(conn, nn, d)
+        P = orc.Pattern.build(conn, nn, d)
+        rp, cs = P.arrays()
+        rrp, rcs = R.pattern()
+        assert np.array_equal(rp, rrp) and np.array_equal(cs, rcs)
+        ed = M.element_dofs(conn, d)
+        K = orc.fill_k(trial, conn.shape[0], ed.shape[1])
+        assert P.assemble_sequential(ed, K).tobytes() == R.assemble(K, "seq", "csr").tobytes()
+        col, _ = R.greedy_colouring(conn.shape[0])
+        assert P.assemble_coloured(ed, K, col).tobytes() == \
+            R.assemble(K, "colour-vec", "csr", threads=2, colour_of=col).tobytes()
+        ones = P.assemble_sequential(ed, np.ones_like(K))
+        assert ones.sum() == conn.shape[0] * ed.shape[1] ** 2
