@@ -99,6 +99,12 @@ struct fea_plan {
     feagpu::DevBuf posE;      // PosT [E*npe*npe] positions, element order (atomic/colour routes; lazy)
     feagpu::DevBuf order;     // int32 [E] atomic-route element order (lazy)
     feagpu::DevBuf node_order;  // int32 [n_own] gather traversal order (empty: node id order)
+    // d = 1 with a traversal order: the sorted incidences re-laid in traversal order, so the
+    // gather reads them sequentially (else: random 128 B line fetches per node)
+    feagpu::DevBuf trav_ptr;   // int64 [n_own+1] record offsets per traversal position
+    feagpu::DevBuf trav_meta;  // int64 [n_own] values start << 20 | row length
+    feagpu::DevBuf trav_rec;   // int32 [n_adj*trav_rw] {entry, position words[, pad]}
+    int32_t trav_rw = 0;
     // colouring
     bool has_colouring = false;
     feagpu::DevBuf colour_elems;           // int32 [E] local elements grouped by colour, ascending id
@@ -111,6 +117,7 @@ struct fea_plan {
     bool gen_on = false;       // fea_assemble_seeded in progress: kernels generate K
     uint64_t gen_seed = 0;
     bool cn_disabled = false;  // FEA_GATHER_NO_CN=1: decode-table gather (A/B)
+    bool d1_disabled = false;  // FEA_GATHER_NO_D1=1: per-node gather for d = 1 (A/B)
     feagpu::DevBuf stage_K, stage_V;       // fea_assemble_host staging
     feagpu::DevBuf bstage_K[2], bstage_V[2];  // fea_assemble_host_batch double buffers
     int64_t kbytes_required() const;

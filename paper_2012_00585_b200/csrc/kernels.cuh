@@ -616,6 +616,138 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_CN_MINB)
 }
 
 // ---------------------------------------------------------------------------
+// Deterministic owner-computes gather for one DOF per node (d = 1): staged incidences
+// ---------------------------------------------------------------------------
+// With d = 1 a node's row block from one element is a single K row of npe doubles (32 B
+// for tet4 / quad4): one sector per incidence and npe adds, so the per-node kernels above
+// are bound by their prologue (order -> adj_ptr -> adj / posA: dependent global loads,
+// then one dependent load per incidence) rather than by HBM. Here a group of G lanes
+// (lane = column, G >= npe) owns one node: the prologue stages the node's incidence
+// records {entry, position words} into shared memory with cp.async (all in flight at
+// once), then the group folds them with PF K rows in flight; one shared load per step
+// yields both the K address and the lane's slot. Groups of a CTA take consecutive
+// traversal nodes (more nodes per group measured slower: the machine's working set then
+// outgrows L2 reuse of the K lines the nodes share). Fold order per slot: ascending
+// element id from the start value (assemble_sequential, assembly.hpp:112-118).
+#ifndef FEA_D1_MINB
+#define FEA_D1_MINB 12
+#endif
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int G, int PF, class PosT, bool DISTINCT, bool GEN>
+__global__ void __launch_bounds__(kWarps * 32, FEA_D1_MINB)
+    k_gather_d1(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
+                const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
+                const int64_t* __restrict__ nptr, const int32_t* __restrict__ order, int64_t n_own,
+                int npe, int pstride, int cap, int rec_stride, int acc_stride, int accumulate, int keep_k_in_l2,
+                const int64_t* __restrict__ tptr, const int64_t* __restrict__ tmeta,
+                const int32_t* __restrict__ trec, GenK gen, double* __restrict__ values) {
+    extern __shared__ double sacc[];
+    constexpr int GPW = 32 / G;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G;
+    const int gw = lane / G;
+    const int grp = (threadIdx.x >> 5) * GPW + gw;
+    const int pw = pstride * static_cast<int>(sizeof(PosT)) / 4;  // position words per incidence
+    const int rw = pw == 1 ? 2 : (pw + 4) & ~3;                   // record words (int2 / int4 aligned)
+    double* acc = sacc + static_cast<int64_t>(grp) * acc_stride;
+    int32_t* rec = reinterpret_cast<int32_t*>(sacc + static_cast<int64_t>(kWarps) * GPW * acc_stride) +
+                   static_cast<int64_t>(grp) * rec_stride;
+
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kWarps * GPW + grp;
+    int64_t a0 = 0, vb = 0;
+    int n = 0, rl = 0;
+    if (tptr != nullptr) {  // records pre-laid in traversal order: sequential reads
+        if (t < n_own) {
+            a0 = tptr[t];
+            n = static_cast<int>(tptr[t + 1] - a0);
+            const int64_t mt = tmeta[t];
+            vb = mt >> 20;
+            rl = static_cast<int>(mt & 0xfffff);
+        }
+        FEA_DCHECK(n <= cap);
+        const int32_t* src = trec + a0 * rw;
+        for (int i = gl; i < n * rw / 2; i += G) cp_async8(rec + 2 * i, src + 2 * i);
+    } else {
+        if (t < n_own) {
+            const int64_t v = order != nullptr ? order[t] : t;
+            a0 = adj_ptr[v];
+            n = static_cast<int>(adj_ptr[v + 1] - a0);
+            vb = nptr[v];
+            rl = static_cast<int>(nptr[v + 1] - vb);
+        }
+        FEA_DCHECK(n <= cap);
+        const uint32_t* pwords = reinterpret_cast<const uint32_t*>(posA + a0 * pstride);
+        for (int i = gl; i < n; i += G) cp_async4(rec + i * rw, adj + a0 + i);
+        for (int i = gl; i < n * pw; i += G) {
+            const int k = i / pw;
+            cp_async4(rec + k * rw + 1 + (i - k * pw), pwords + i);
+        }
+    }
+    for (int i = gl; i < rl; i += G) acc[i] = accumulate ? values[vb + i] : 0.0;
+    cp_async_wait_all();
+    __syncwarp();
+    const int n_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
+
+    const bool col_ok = gl < npe;
+    // incidence k: element-matrix row (entry) and this lane's slot
+    auto record = [&](int k, int32_t& entry) -> int {
+        if (pw == 1) {
+            const int2 r = *reinterpret_cast<const int2*>(rec + 2 * k);
+            entry = r.x;
+            constexpr int B = 8 * sizeof(PosT);
+            return static_cast<int>((static_cast<uint32_t>(r.y) >> (B * gl)) & ((1u << B) - 1u));
+        }
+        entry = rec[k * rw];
+        return static_cast<int>(reinterpret_cast<const PosT*>(rec + k * rw + 1)[gl]);
+    };
+    double kv[PF];
+    int q[PF];
+    auto load = [&](int p, int k) {
+        if (k < n && col_ok) {
+            int32_t entry;
+            q[p] = record(k, entry);
+            if (GEN) {
+                const int64_t krow = entry / npe;
+                const int a = static_cast<int>(entry - krow * npe);
+                kv[p] = kgen_entry(kgen_elem(gen.seed, gen.ids ? gen.ids[krow] : krow), a, gl);
+            } else {
+                const double* src = K + static_cast<int64_t>(entry) * npe + gl;
+                kv[p] = keep_k_in_l2 ? __ldcg(src) : ld_stream(src);
+            }
+        }
+    };
+#pragma unroll
+    for (int p = 0; p < PF; ++p) load(p, p);
+    for (int k0 = 0; k0 < n_max; k0 += PF) {
+#pragma unroll
+        for (int p = 0; p < PF; ++p) {
+            const int k = k0 + p;
+            if (DISTINCT) {
+                if (k < n && col_ok) {
+                    FEA_DCHECK(q[p] < rl);
+                    acc[q[p]] += kv[p];
+                }
+            } else {  // a repeated node: columns share a slot, folded lane by lane
+                for (int l = 0; l < G; ++l) {
+                    if (k < n && col_ok && gl == l) acc[q[p]] += kv[p];
+                    __syncwarp();
+                }
+            }
+            __syncwarp();
+            load(p, k + PF);
+        }
+    }
+    for (int i = gl; i < rl; i += G) __stcs(values + vb + i, acc[i]);
+}
+
+// ---------------------------------------------------------------------------
 // Element-owner scatter: atomics (FEA_ATOMIC) or plain adds within a colour
 // ---------------------------------------------------------------------------
 // tab[idx] = a | ki<<8 | b<<16 | kj<<24 for idx = i*m + j, i = a*d+ki, j = b*d+kj.
@@ -869,12 +1001,61 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
     p->last_launches += 1;
 }
 
+template <int G, int PF, class PosT>
+void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
+                   cudaStream_t s) {
+    constexpr int GPW = 32 / G;
+    // accumulator stride = 3 (mod 16 doubles): swept all odd residues on cfg3, 3 fewest conflicts
+    // (0.642 ms vs 0.664 at 15 and 0.670 at 1)
+    int acc_stride = std::max(p->max_cnt, 1);
+    int acc_mod = 3;
+    if (const char* e = std::getenv("FEA_D1_ACC_STRIDE_MOD16")) acc_mod = std::atoi(e) & 15;
+    while ((acc_stride & 15) != acc_mod) ++acc_stride;
+    const int cap = static_cast<int>(std::max<int64_t>(p->max_adj, 1));
+    const int pw = p->pstride * static_cast<int>(sizeof(PosT)) / 4;
+    const int rw = pw == 1 ? 2 : (pw + 4) & ~3;
+    // per-group record stride in words with stride/2 odd: the 8 groups' 8-byte record reads
+    // of one step land on 8 distinct bank pairs
+    int rec_stride = cap * rw;
+    if (((rec_stride / 2) & 1) == 0) rec_stride += 2;
+    const size_t smem = static_cast<size_t>(kWarps) * GPW *
+                        (acc_stride * sizeof(double) + static_cast<size_t>(rec_stride) * sizeof(int32_t));
+    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
+    auto kern = p->gen_on ? (p->dup_nodes ? k_gather_d1<G, PF, PosT, false, true> : k_gather_d1<G, PF, PosT, true, true>)
+                          : (p->dup_nodes ? k_gather_d1<G, PF, PosT, false, false> : k_gather_d1<G, PF, PosT, true, false>);
+    if (smem > 48 * 1024)
+        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t per_cta = static_cast<int64_t>(kWarps) * GPW;
+    const int64_t blocks = (p->n_own + per_cta - 1) / per_cta;
+    if (blocks == 0) return;
+    // traversal-ordered records exist for the sorted incidences only (not the colour order)
+    const bool trav = p->trav_rec.p != nullptr && in.adj == p->adj.as<int32_t>();
+    FEA_REQUIRE(!trav || p->trav_rw == rw, FEA_ERR_INVALID, "traversal record width mismatch");
+    kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
+        K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const PosT*>(in.posA), p->nptr.as<int64_t>(),
+        p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, p->npe, p->pstride, cap,
+        rec_stride, acc_stride, accumulate ? 1 : 0, p->m * 8 < 128 ? 1 : 0, trav ? p->trav_ptr.as<int64_t>() : nullptr,
+        trav ? p->trav_meta.as<int64_t>() : nullptr, trav ? p->trav_rec.as<int32_t>() : nullptr, gen_of(p), values);
+    FEA_CK(cudaGetLastError());
+    p->last_launches += 1;
+}
+
 template <class PosT>
 void gather(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
             cudaStream_t s) {
     const int dm = p->d * p->m;
     // lane = column node (d in {2,3,4}, npe <= 32); measured faster than the decode-table
     // kernels for every such shape
+    // d = 1: staged-stream kernel
+    if (!p->d1_disabled && p->d == 1 && p->npe <= 32) {
+#ifndef FEA_D1_PF
+#define FEA_D1_PF 4  // swept 2-12 on cfg3: 3-4 best
+#endif
+        if (p->npe <= 4) return run_gather_d1<4, FEA_D1_PF, PosT>(p, in, K, values, accumulate, s);
+        if (p->npe <= 8) return run_gather_d1<8, FEA_D1_PF, PosT>(p, in, K, values, accumulate, s);
+        if (p->npe <= 16) return run_gather_d1<16, 4, PosT>(p, in, K, values, accumulate, s);
+        return run_gather_d1<32, 4, PosT>(p, in, K, values, accumulate, s);
+    }
     if (!p->cn_disabled && p->d >= 2 && p->d <= 4 && p->npe <= 32) {
         const int G = p->npe <= 4 ? 4 : p->npe <= 8 ? 8 : p->npe <= 16 ? 16 : 32;
         switch (G * 10 + p->d) {

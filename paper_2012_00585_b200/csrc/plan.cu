@@ -740,6 +740,68 @@ void build_node_order(fea_plan* p, cudaStream_t s) {
     FEA_CK(cudaStreamSynchronize(s));
 }
 
+__global__ void k_trav_count(const int32_t* __restrict__ order, const int64_t* __restrict__ adj_ptr,
+                             const int64_t* __restrict__ nptr, int64_t n_own, int64_t* __restrict__ cnt,
+                             int64_t* __restrict__ meta) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_own;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = order[t];
+        cnt[t] = adj_ptr[v + 1] - adj_ptr[v];
+        meta[t] = (nptr[v] << 20) | (nptr[v + 1] - nptr[v]);
+    }
+}
+
+__global__ void k_trav_records(const int32_t* __restrict__ order, const int64_t* __restrict__ adj_ptr,
+                               const int32_t* __restrict__ adj, const uint32_t* __restrict__ pos_words,
+                               int pw, int rw, const int64_t* __restrict__ tptr, int64_t n_own,
+                               int32_t* __restrict__ rec) {
+    // one warp per traversal position: lanes copy the node's records
+    const int lane = threadIdx.x & 31;
+    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n_own;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t v = order[t];
+        const int64_t a0 = adj_ptr[v], n = adj_ptr[v + 1] - a0, r0 = tptr[t];
+        for (int64_t k = lane; k < n; k += 32) {
+            int32_t* r = rec + (r0 + k) * rw;
+            r[0] = adj[a0 + k];
+            for (int w = 0; w < pw; ++w) r[1 + w] = static_cast<int32_t>(pos_words[(a0 + k) * pw + w]);
+            for (int w = pw + 1; w < rw; ++w) r[w] = 0;
+        }
+    }
+}
+
+// d = 1 sorted gather with a traversal order: incidence records in traversal order
+void build_traversal(fea_plan* p, cudaStream_t s) {
+    p->trav_ptr.reset();
+    p->trav_meta.reset();
+    p->trav_rec.reset();
+    if (!p->node_order.p || p->d != 1 || p->npe > 32 || p->d1_disabled || std::getenv("FEA_NO_TRAVERSAL_RECORDS"))
+        return;
+    const int pw = p->pstride * p->pos_bytes / 4;
+    const int rw = pw == 1 ? 2 : (pw + 4) & ~3;
+    DevBuf cnt;
+    cnt.alloc((p->n_own + 1) * 8);
+    FEA_CK(cudaMemsetAsync(cnt.p, 0, cnt.bytes, s));
+    p->trav_meta.alloc(p->n_own * 8);
+    k_trav_count<<<grid_for(p->n_own, 256), 256, 0, s>>>(p->node_order.as<int32_t>(), p->adj_ptr.as<int64_t>(),
+                                                         p->nptr.as<int64_t>(), p->n_own, cnt.as<int64_t>(),
+                                                         p->trav_meta.as<int64_t>());
+    FEA_CK(cudaGetLastError());
+    p->trav_ptr.alloc((p->n_own + 1) * 8);
+    cub_call([&](void* t, size_t& tb) {
+        return cub::DeviceScan::ExclusiveSum(t, tb, cnt.as<int64_t>(), p->trav_ptr.as<int64_t>(),
+                                             (int)(p->n_own + 1), s);
+    });
+    p->trav_rec.alloc(std::max<int64_t>(p->n_adj, 1) * rw * 4);
+    k_trav_records<<<grid_for(p->n_own * 32, 256), 256, 0, s>>>(
+        p->node_order.as<int32_t>(), p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(),
+        static_cast<const uint32_t*>(p->posA.p), pw, rw, p->trav_ptr.as<int64_t>(), p->n_own,
+        p->trav_rec.as<int32_t>());
+    FEA_CK(cudaGetLastError());
+    p->trav_rw = rw;
+    FEA_CK(cudaStreamSynchronize(s));
+}
+
 void build_runs(fea_plan* p, cudaStream_t s) {
     DevBuf runs;
     runs.alloc((p->n_own + 1) * sizeof(int64_t));
@@ -824,6 +886,7 @@ void build_own_pattern(fea_plan* p, cudaStream_t s) {
     }
     build_runs(p, s);
     build_node_order(p, s);
+    build_traversal(p, s);
 }
 
 // Common front end: DOFs -> node connectivity (with node-layout detection),
@@ -1007,7 +1070,8 @@ int64_t metadata_bytes(const fea_plan* p) {
                                 p->adj_ptr.bytes + p->adj.bytes + p->nptr.bytes + p->ncol.bytes +
                                 p->nrun_ptr.bytes + p->posA.bytes + p->posE.bytes +
                                 p->order.bytes + p->colour_elems.bytes + p->adjC.bytes + p->posAC.bytes +
-                                p->node_order.bytes);
+                                p->node_order.bytes + p->trav_ptr.bytes + p->trav_meta.bytes +
+                                p->trav_rec.bytes);
 }
 
 }  // namespace feagpu
@@ -1039,6 +1103,7 @@ fea_status fea_plan_create(int device, const int64_t* elem_dofs, int64_t n_eleme
         auto p = std::make_unique<fea_plan>();
         p->device = device;
         p->cn_disabled = std::getenv("FEA_GATHER_NO_CN") != nullptr;
+        p->d1_disabled = std::getenv("FEA_GATHER_NO_D1") != nullptr;
         p->E_in = n_elements;
         p->m = m;
         p->n_rows = n_rows;
@@ -1183,6 +1248,7 @@ fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, in
         }
         build_runs(p.get(), s);
         build_node_order(p.get(), s);
+        build_traversal(p.get(), s);
         FEA_CK(cudaStreamSynchronize(s));
         *out = p.release();
     });

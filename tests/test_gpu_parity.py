@@ -119,16 +119,18 @@ def test_accumulate_twice_doubles(gpu, orc, strategy):
         assert torch.equal(v, 2 * once)
 
 
-def test_accumulate_is_left_fold_from_existing(gpu, orc):
+@pytest.mark.parametrize("mesh,n,d,perm", [("hex8", 3, 3, "elements"), ("tet4", 4, 1, "nodes"),
+                                            ("quad4", 6, 1, None)])
+def test_accumulate_is_left_fold_from_existing(gpu, orc, mesh, n, d, perm):
     """FEA_ACCUMULATE on the sorted route continues the fold from the slot's value,
     exactly like assemble_sequential on a non-reset target."""
     import torch
-    conn, nn, ed, n_rows = problem("hex8", 3, 3, "elements")
-    P = orc.Pattern.build(conn, nn, 3)
+    conn, nn, ed, n_rows = problem(mesh, n, d, perm)
+    P = orc.Pattern.build(conn, nn, d)
     Kh = orc.fill_k(5, conn.shape[0], ed.shape[1])
     start = orc.fill_k(9, 1, int(np.ceil(np.sqrt(P.nnz))))[0].reshape(-1)[: P.nnz].copy()
     want = P.assemble_sequential(ed, Kh, start.copy())
-    with gpu.Plan(ed, n_rows, dofs_per_node=3) as plan:
+    with gpu.Plan(ed, n_rows, dofs_per_node=d) as plan:
         v = torch.from_numpy(start.copy()).cuda()
         plan.assemble(torch.from_numpy(Kh).cuda(), v, strategy="sorted", accumulate=True)
         assert v.cpu().numpy().tobytes() == want.tobytes()
@@ -191,18 +193,20 @@ def test_invalid_colouring_rejected(gpu):
 
 
 @pytest.mark.parametrize("k_compact", [False, True])
-def test_row_partition_blocks_concatenate(gpu, orc, k_compact):
+@pytest.mark.parametrize("mesh,n,d,perm", [("hex8", 4, 3, "elements"), ("tet4", 4, 1, "nodes")])
+def test_row_partition_blocks_concatenate(gpu, orc, k_compact, mesh, n, d, perm):
     """Row-partitioned plans: each owned block's CSR/CRAC/values equal the matching slice
-    of the whole-matrix result."""
+    of the whole-matrix result. tet4 d=1 with permuted node ids runs the
+    traversal-ordered d = 1 gather on each block."""
     import torch
-    conn, nn, ed, n_rows = problem("hex8", 4, 3, "elements")
-    P = orc.Pattern.build(conn, nn, 3)
+    conn, nn, ed, n_rows = problem(mesh, n, d, perm)
+    P = orc.Pattern.build(conn, nn, d)
     rp, cs = P.arrays()
     Kh = orc.fill_k(42, conn.shape[0], ed.shape[1])
     want = P.assemble_sequential(ed, Kh)
-    cuts = [0, 3 * 40, 3 * 41, 3 * 90, n_rows]
+    cuts = [0, d * 40, d * 41, d * 90, n_rows]
     for rb, re in zip(cuts[:-1], cuts[1:]):
-        with gpu.Plan(ed, n_rows, dofs_per_node=3, row_range=(rb, re), k_compact=k_compact) as plan:
+        with gpu.Plan(ed, n_rows, dofs_per_node=d, row_range=(rb, re), k_compact=k_compact) as plan:
             prp, pcs = plan.csr()
             assert np.array_equal(prp, rp[rb:re + 1] - rp[rb])
             assert np.array_equal(pcs, cs[rp[rb]:rp[re]])

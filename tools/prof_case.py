@@ -29,6 +29,9 @@ if "colour" in strategies:
     plan.set_colouring(plan.greedy_colouring()[0])
 for s in strategies:
     for _ in range(a.iters):
-        plan.assemble(K, v, strategy=s, accumulate=s != "sorted")
+        if s == "fused":
+            plan.assemble_seeded(42, v, strategy="sorted")
+        else:
+            plan.assemble(K, v, strategy=s, accumulate=s != "sorted")
 torch.cuda.synchronize()
 print("ok", plan.nnz, plan.n_runs)
