@@ -283,8 +283,9 @@ def run_ours(args):
     my_ms = total_ms / args.steps
     peak, peak_src = measured_peak_gbs()
     achieved = min_bytes / (my_ms * 1e-3) / 1e9
-    kernel_name = {"sorted": "k_gather_cn<8,3,2,u8> (lane = column node)", "atomic": "k_scatter<32,u8,atomic>",
-                   "colour": "k_gather_cn<8,3,2,u8> (colour-ordered incidences)",
+    kernel_name = {"sorted": "k_gather_slot<3,8> (warp = node, lane = slot, register accumulators)",
+                   "atomic": "k_scatter<32,u8,atomic>",
+                   "colour": "k_gather_slot<3,8> (colour-ordered incidences)",
                    "colour_passes": "k_scatter<32,u8,plain> x n_colours"}[args.strategy]
     traffic = profiled_traffic(f"cfg2/{args.strategy}") if N == 1 else None
 

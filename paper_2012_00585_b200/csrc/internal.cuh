@@ -118,6 +118,7 @@ struct fea_plan {
     uint64_t gen_seed = 0;
     bool cn_disabled = false;  // FEA_GATHER_NO_CN=1: decode-table gather (A/B)
     bool d1_disabled = false;  // FEA_GATHER_NO_D1=1: per-node gather for d = 1 (A/B)
+    bool slot_disabled = false;  // FEA_GATHER_NO_SLOT=1: column-node gather for d in 2..4 (A/B)
     feagpu::DevBuf stage_K, stage_V;       // fea_assemble_host staging
     feagpu::DevBuf bstage_K[2], bstage_V[2];  // fea_assemble_host_batch double buffers
     int64_t kbytes_required() const;

@@ -748,6 +748,204 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_D1_MINB)
 }
 
 // ---------------------------------------------------------------------------
+// Deterministic owner-computes gather, lane = slot (d in {2,3,4}, npe <= 8, rows <= 32 nodes)
+// ---------------------------------------------------------------------------
+// The shared-memory accumulator of the kernels above costs a read-add-write per entry
+// at data-dependent slots; on cfg2 those wavefronts (with bank conflicts) keep the L1 data
+// pipe ~92 % busy. Here a WARP owns a node and lane s owns column node s of the node's row:
+// its d x d values live in registers. The node's incident element row blocks ("chunks",
+// d*m doubles each) are copied whole into shared memory with 16-byte cp.async (coalesced,
+// no registers, all of a node's chunks in flight at once, double-buffered one node ahead);
+// per chunk, lane s finds the element column that lands in its slot (byte compare on the
+// position word) and adds that column's d x d sub-block from shared memory. Warps take
+// nodes w, w + W, w + 2W, ... so the machine works on a contiguous window of nodes (the
+// half lines two chunks of one element share stay in L2). Fold order per slot: ascending
+// element id from the start value, then (repeated nodes) ascending column —
+// assemble_sequential order (assembly.hpp:112-118), bit for bit.
+#ifndef FEA_SLOT_MINB
+#define FEA_SLOT_MINB 6  // swept 4 (95 regs) 0.318 ms, 6 0.303, 8 0.305 on cfg2
+#endif
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <int D, int NPE, bool DISTINCT, bool GEN>
+__global__ void __launch_bounds__(kWarps * 32, FEA_SLOT_MINB)
+    k_gather_slot(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
+                  const int32_t* __restrict__ adj, const uint8_t* __restrict__ posA,
+                  const int64_t* __restrict__ nptr, const int32_t* __restrict__ order, int64_t n_own,
+                  int nbuf, int accumulate, GenK gen, double* __restrict__ values) {
+    extern __shared__ double sbuf[];
+    constexpr int PW = NPE <= 4 ? 1 : 2;  // position words per incidence
+    constexpr int npe = NPE;
+    constexpr int m = D * NPE;
+    constexpr int dm = D * m;     // doubles per chunk (even: 16-byte pieces)
+    constexpr int half = dm / 2;  // 16-byte pieces per chunk
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    double* wbuf = sbuf + static_cast<int64_t>(warp) * 2 * nbuf * dm;
+    const int64_t W = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+
+    // per-node pipeline: incidence range 3 nodes ahead, records (entry, position words) and
+    // row info 2 ahead, chunk copies 1 ahead, fold of the current node
+    struct Ptr {
+        int64_t a0;
+        int n;
+    };
+    auto ptr_of = [&](int64_t t) -> Ptr {
+        Ptr P{0, 0};
+        if (t < n_own) {
+            const int64_t v = order != nullptr ? order[t] : t;
+            P.a0 = adj_ptr[v];
+            P.n = static_cast<int>(adj_ptr[v + 1] - P.a0);
+        }
+        return P;
+    };
+    struct Rec {
+        int32_t ent;       // lane k: entry of incidence k
+        uint32_t pw[PW];   // lane k: position words of incidence k
+        int64_t c0;        // node row info (warp-uniform)
+        int cnt, n;
+    };
+    auto rec_of = [&](const Ptr& P, int64_t t) -> Rec {
+        Rec R;
+        R.ent = 0;
+#pragma unroll
+        for (int w = 0; w < PW; ++w) R.pw[w] = 0;
+        R.n = P.n;
+        R.c0 = 0;
+        R.cnt = 0;
+        if (t < n_own) {
+            const int64_t v = order != nullptr ? order[t] : t;
+            R.c0 = nptr[v];
+            R.cnt = static_cast<int>(nptr[v + 1] - R.c0);
+        }
+        if (lane < P.n) {
+            R.ent = adj[P.a0 + lane];
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(posA) + (P.a0 + lane) * PW;
+#pragma unroll
+            for (int w = 0; w < PW; ++w) R.pw[w] = src[w];
+        }
+        return R;
+    };
+    auto issue = [&](const Rec& R, int b) {
+        if (!GEN) {
+            double* dst = wbuf + static_cast<int64_t>(b) * nbuf * dm;
+            for (int k = 0; k < R.n; ++k) {  // chunk k: lanes copy its 16-byte pieces
+                const int32_t e = __shfl_sync(0xffffffffu, R.ent, k);
+                const double* src = K + static_cast<int64_t>(e) * dm;
+#pragma unroll
+                for (int pc = lane; pc < half; pc += 32) cp_async16(dst + k * dm + 2 * pc, src + 2 * pc);
+            }
+        }
+        cp_async_commit();
+    };
+    // per-warp inverse position table: inv[k*32 + slot] = element column + 1 (0: none)
+    uint8_t* inv = reinterpret_cast<uint8_t*>(sbuf + static_cast<int64_t>(kWarps) * 2 * nbuf * dm) +
+                   static_cast<int64_t>(warp) * nbuf * 32;
+    const uint32_t key = static_cast<uint32_t>(lane) * 0x01010101u;
+    uint32_t valid[PW];
+#pragma unroll
+    for (int w = 0; w < PW; ++w) {
+        const int nb = npe - 4 * w;
+        valid[w] = nb >= 4 ? 0xffffffffu : nb <= 0 ? 0u : ((1u << (8 * nb)) - 1u);
+    }
+
+    Rec Rc = rec_of(ptr_of(t0), t0);            // node j
+    Rec R1 = rec_of(ptr_of(t0 + W), t0 + W);    // node j + 1
+    Ptr P2 = ptr_of(t0 + 2 * W);                // node j + 2
+    issue(Rc, 0);
+    int b = 0;
+    for (int64_t t = t0; t < n_own; t += W) {
+        const Ptr P3 = ptr_of(t + 3 * W);
+        const Rec R2 = rec_of(P2, t + 2 * W);
+        issue(R1, b ^ 1);   // node j + 1's chunks, overlapping node j's fold
+        cp_async_wait_1();  // node j's chunks have landed (this lane's pieces)
+        __syncwarp();
+        const double* cb = wbuf + static_cast<int64_t>(b) * nbuf * dm;
+        const bool mine = lane < Rc.cnt;
+        const int rowlen = D * Rc.cnt;
+        double* vrow = values + static_cast<int64_t>(D) * D * Rc.c0 + lane * D;
+        double acc[D][D];
+#pragma unroll
+        for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+            for (int kj = 0; kj < D; ++kj) acc[ki][kj] = (accumulate && mine) ? vrow[ki * rowlen + kj] : 0.0;
+        if constexpr (DISTINCT && !GEN) {
+            // slots of one element are distinct: invert the position bytes once per node
+            uint32_t* inv32 = reinterpret_cast<uint32_t*>(inv);
+            for (int i = lane; i < Rc.n * 8; i += 32) inv32[i] = 0u;
+            __syncwarp();
+            for (int base = 0; base < Rc.n * NPE; base += 32) {  // warp-uniform trip count (shuffles)
+                const int q = base + lane;
+                const int k = q / NPE, col = q - k * NPE;
+                // shuffle every word, then select: the source lane evaluates the shuffled operand
+                const uint32_t w0 = __shfl_sync(0xffffffffu, Rc.pw[0], k & 31);
+                const uint32_t w1 = PW == 1 ? w0 : __shfl_sync(0xffffffffu, Rc.pw[PW - 1], k & 31);
+                const uint32_t w = col < 4 ? w0 : w1;
+                if (q < Rc.n * NPE) inv[k * 32 + ((w >> (8 * (col & 3))) & 0xffu)] = static_cast<uint8_t>(col + 1);
+            }
+            __syncwarp();
+            if (mine) {
+                for (int k = 0; k < Rc.n; ++k) {
+                    const int c = inv[k * 32 + lane];
+                    if (c) {
+                        const double* src = cb + k * dm + (c - 1) * D;
+#pragma unroll
+                        for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+                            for (int kj = 0; kj < D; ++kj) acc[ki][kj] += src[ki * m + kj];
+                    }
+                }
+            }
+        } else
+        for (int k = 0; k < Rc.n; ++k) {
+            // bit 8*col set when element column node col lands in this lane's slot
+            uint64_t mm = __vcmpeq4(__shfl_sync(0xffffffffu, Rc.pw[0], k), key) & valid[0] & 0x01010101u;
+            if (PW == 2)
+                mm |= static_cast<uint64_t>(__vcmpeq4(__shfl_sync(0xffffffffu, Rc.pw[PW - 1], k), key) &
+                                            valid[PW - 1] & 0x01010101u) << 32;
+            const int32_t e = GEN ? __shfl_sync(0xffffffffu, Rc.ent, k) : 0;
+            if (!mine) continue;
+            for (; mm; mm &= mm - 1) {  // DISTINCT: at most one column per slot
+                const int col = (__ffsll(static_cast<long long>(mm)) - 1) >> 3;
+                if (GEN) {
+                    const int64_t krow = e / npe;
+                    const int a = static_cast<int>(e - krow * npe);
+                    const uint64_t he = kgen_elem(gen.seed, gen.ids ? gen.ids[krow] : krow);
+#pragma unroll
+                    for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+                        for (int kj = 0; kj < D; ++kj) acc[ki][kj] += kgen_entry(he, a * D + ki, col * D + kj);
+                } else {
+                    const double* src = cb + k * dm + col * D;
+#pragma unroll
+                    for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+                        for (int kj = 0; kj < D; ++kj) acc[ki][kj] += src[ki * m + kj];
+                }
+                if (DISTINCT) break;
+            }
+        }
+        if (mine) {
+#pragma unroll
+            for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+                for (int kj = 0; kj < D; ++kj) __stcs(vrow + ki * rowlen + kj, acc[ki][kj]);
+        }
+        __syncwarp();  // buffer b is refilled two nodes on
+        Rc = R1;
+        R1 = R2;
+        P2 = P3;
+        b ^= 1;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
 // Element-owner scatter: atomics (FEA_ATOMIC) or plain adds within a colour
 // ---------------------------------------------------------------------------
 // tab[idx] = a | ki<<8 | b<<16 | kj<<24 for idx = i*m + j, i = a*d+ki, j = b*d+kj.
@@ -973,6 +1171,42 @@ void run_gather(fea_plan* p, const Incidences& in, const double* K, double* valu
     else run_gather_node<G, R, PF, PosT>(p, in, K, values, accumulate, s);
 }
 
+template <int D, int NPE>
+void run_gather_slot(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
+                     cudaStream_t s) {
+    const int dm = D * D * NPE;
+    const int nbuf = static_cast<int>(std::max<int64_t>(p->max_adj, 1));
+    const size_t smem = static_cast<size_t>(kWarps) * nbuf * (2 * dm * sizeof(double) + 32);
+    auto kern = p->gen_on ? (p->dup_nodes ? k_gather_slot<D, NPE, false, true> : k_gather_slot<D, NPE, true, true>)
+                          : (p->dup_nodes ? k_gather_slot<D, NPE, false, false> : k_gather_slot<D, NPE, true, false>);
+    if (smem > 48 * 1024)
+        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, sms = 148, per_sm = 1;
+    FEA_CK(cudaGetDevice(&dev));
+    FEA_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FEA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem));
+    const int64_t want = (p->n_own + kWarps - 1) / kWarps;  // one node per warp at most
+    const int64_t blocks = std::min<int64_t>(want, static_cast<int64_t>(sms) * std::max(per_sm, 1));
+    if (blocks == 0) return;
+    kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
+        K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const uint8_t*>(in.posA), p->nptr.as<int64_t>(),
+        p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, nbuf, accumulate ? 1 : 0,
+        gen_of(p), values);
+    FEA_CK(cudaGetLastError());
+    p->last_launches += 1;
+}
+
+// lane = slot kernel applies: d in {2,3,4}, element rows of <= 8 nodes with byte positions,
+// node rows of <= 32 column nodes, <= 32 incidences per node, 16-byte chunks, <= 96 KB smem
+bool slot_applies(const fea_plan* p) {
+    if (p->d < 2 || p->d > 4 || (p->npe != 4 && p->npe != 8) || p->pos_bytes != 1 || p->max_cnt > 32 ||
+        p->max_adj > 32 || p->gen_on)
+        return false;
+    const int64_t dm = static_cast<int64_t>(p->d) * p->d * p->npe;
+    if (dm % 2) return false;
+    return static_cast<int64_t>(kWarps) * 2 * std::max<int64_t>(p->max_adj, 1) * dm * 8 <= 96 * 1024;
+}
+
 #ifndef FEA_CN_PF8
 #define FEA_CN_PF8 2
 #endif
@@ -1055,6 +1289,14 @@ void gather(fea_plan* p, const Incidences& in, const double* K, double* values, 
         if (p->npe <= 8) return run_gather_d1<8, FEA_D1_PF, PosT>(p, in, K, values, accumulate, s);
         if (p->npe <= 16) return run_gather_d1<16, 4, PosT>(p, in, K, values, accumulate, s);
         return run_gather_d1<32, 4, PosT>(p, in, K, values, accumulate, s);
+    }
+    if (!p->slot_disabled && slot_applies(p)) {
+        const bool n4 = p->npe == 4;
+        switch (p->d) {
+            case 2: return n4 ? run_gather_slot<2, 4>(p, in, K, values, accumulate, s) : run_gather_slot<2, 8>(p, in, K, values, accumulate, s);
+            case 3: return n4 ? run_gather_slot<3, 4>(p, in, K, values, accumulate, s) : run_gather_slot<3, 8>(p, in, K, values, accumulate, s);
+            default: return n4 ? run_gather_slot<4, 4>(p, in, K, values, accumulate, s) : run_gather_slot<4, 8>(p, in, K, values, accumulate, s);
+        }
     }
     if (!p->cn_disabled && p->d >= 2 && p->d <= 4 && p->npe <= 32) {
         const int G = p->npe <= 4 ? 4 : p->npe <= 8 ? 8 : p->npe <= 16 ? 16 : 32;

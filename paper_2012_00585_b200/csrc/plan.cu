@@ -1104,6 +1104,7 @@ fea_status fea_plan_create(int device, const int64_t* elem_dofs, int64_t n_eleme
         p->device = device;
         p->cn_disabled = std::getenv("FEA_GATHER_NO_CN") != nullptr;
         p->d1_disabled = std::getenv("FEA_GATHER_NO_D1") != nullptr;
+        p->slot_disabled = std::getenv("FEA_GATHER_NO_SLOT") != nullptr;
         p->E_in = n_elements;
         p->m = m;
         p->n_rows = n_rows;
