@@ -762,6 +762,9 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_D1_MINB)
 // half lines two chunks of one element share stay in L2). Fold order per slot: ascending
 // element id from the start value, then (repeated nodes) ascending column —
 // assemble_sequential order (assembly.hpp:112-118), bit for bit.
+#ifndef FEA_SLOT_TMA
+#define FEA_SLOT_TMA 1
+#endif
 #ifndef FEA_SLOT_MINB
 #define FEA_SLOT_MINB 6  // swept 4 (95 regs) 0.318 ms, 6 0.303, 8 0.305 on cfg2
 #endif
@@ -831,6 +834,43 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_SLOT_MINB)
         }
         return R;
     };
+    // per-warp inverse position table: inv[k*32 + slot] = element column + 1 (0: none)
+    uint8_t* inv = reinterpret_cast<uint8_t*>(sbuf + static_cast<int64_t>(kWarps) * 2 * nbuf * dm) +
+                   static_cast<int64_t>(warp) * nbuf * 32;
+#if FEA_SLOT_TMA
+    // one mbarrier per buffer; lane k issues block k as ONE bulk copy (TMA), completion by bytes
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sbuf) +
+                                                 static_cast<int64_t>(kWarps) * nbuf * (2 * dm * 8 + 32)) +
+                     2 * warp;
+    if (!GEN && lane == 0) {
+        mbar_init(smem_u32(bars), 1);
+        mbar_init(smem_u32(bars + 1), 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    uint32_t phase = 0;  // bit b: parity of buffer b's next completion
+    auto issue = [&](const Rec& R, int b) {
+        if (!GEN) {
+            if (lane == 0) mbar_arrive_expect_tx(smem_u32(bars + b), static_cast<uint32_t>(R.n * dm * 8));
+            __syncwarp();
+            if (lane < R.n) {
+                fence_proxy_async_smem();  // buffer b was last read by generic loads two nodes ago
+                double* dst = wbuf + static_cast<int64_t>(b) * nbuf * dm + lane * dm;
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(dst)),
+                    "l"(K + static_cast<int64_t>(R.ent) * dm), "r"(dm * 8), "r"(smem_u32(bars + b))
+                    : "memory");
+            }
+        }
+    };
+    auto wait_blocks = [&](int b) {
+        if (!GEN) {
+            mbar_wait(smem_u32(bars + b), (phase >> b) & 1u);
+            phase ^= 1u << b;
+        }
+    };
+#else
     auto issue = [&](const Rec& R, int b) {
         if (!GEN) {
             double* dst = wbuf + static_cast<int64_t>(b) * nbuf * dm;
@@ -843,9 +883,8 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_SLOT_MINB)
         }
         cp_async_commit();
     };
-    // per-warp inverse position table: inv[k*32 + slot] = element column + 1 (0: none)
-    uint8_t* inv = reinterpret_cast<uint8_t*>(sbuf + static_cast<int64_t>(kWarps) * 2 * nbuf * dm) +
-                   static_cast<int64_t>(warp) * nbuf * 32;
+    auto wait_blocks = [&](int) { cp_async_wait_1(); };  // all but the newest group
+#endif
     const uint32_t key = static_cast<uint32_t>(lane) * 0x01010101u;
     uint32_t valid[PW];
 #pragma unroll
@@ -863,7 +902,7 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_SLOT_MINB)
         const Ptr P3 = ptr_of(t + 3 * W);
         const Rec R2 = rec_of(P2, t + 2 * W);
         issue(R1, b ^ 1);   // node j + 1's chunks, overlapping node j's fold
-        cp_async_wait_1();  // node j's chunks have landed (this lane's pieces)
+        wait_blocks(b);     // node j's chunks have landed
         __syncwarp();
         const double* cb = wbuf + static_cast<int64_t>(b) * nbuf * dm;
         const bool mine = lane < Rc.cnt;
@@ -1176,7 +1215,7 @@ void run_gather_slot(fea_plan* p, const Incidences& in, const double* K, double*
                      cudaStream_t s) {
     const int dm = D * D * NPE;
     const int nbuf = static_cast<int>(std::max<int64_t>(p->max_adj, 1));
-    const size_t smem = static_cast<size_t>(kWarps) * nbuf * (2 * dm * sizeof(double) + 32);
+    const size_t smem = static_cast<size_t>(kWarps) * nbuf * (2 * dm * sizeof(double) + 32) + kWarps * 16;
     auto kern = p->gen_on ? (p->dup_nodes ? k_gather_slot<D, NPE, false, true> : k_gather_slot<D, NPE, true, true>)
                           : (p->dup_nodes ? k_gather_slot<D, NPE, false, false> : k_gather_slot<D, NPE, true, false>);
     if (smem > 48 * 1024)
@@ -1290,7 +1329,8 @@ void gather(fea_plan* p, const Incidences& in, const double* K, double* values, 
         if (p->npe <= 16) return run_gather_d1<16, 4, PosT>(p, in, K, values, accumulate, s);
         return run_gather_d1<32, 4, PosT>(p, in, K, values, accumulate, s);
     }
-    if (!p->slot_disabled && slot_applies(p)) {
+    // (bulk copies need 16-byte aligned element matrices)
+    if (!p->slot_disabled && slot_applies(p) && (reinterpret_cast<uintptr_t>(K) & 15) == 0) {
         const bool n4 = p->npe == 4;
         switch (p->d) {
             case 2: return n4 ? run_gather_slot<2, 4>(p, in, K, values, accumulate, s) : run_gather_slot<2, 8>(p, in, K, values, accumulate, s);
