@@ -233,7 +233,7 @@ def run_ours(args):
                 values.zero_()
             one(strategy, acc)
         if sampler is not None:  # soak so the clock samples see the GPU under this load
-            t_end = time.perf_counter() + 1.5
+            t_end = time.perf_counter() + float(os.environ.get("FEA_BENCH_SOAK_S", "1.5"))
             while time.perf_counter() < t_end:
                 for _ in range(20):
                     one(strategy, acc)

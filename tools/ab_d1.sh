@@ -1,3 +1,5 @@
 #!/bin/bash
-python -m pytest tests -m gpu -x -q > gpurun_out/t.log 2>&1 || { tail -30 gpurun_out/t.log; exit 1; }
-timeout 600 python tools/bench_configs.py --configs 1,2,3,4 --runs 5 --oracle > gpurun_out/configs.jsonl 2>gpurun_out/configs.err
+# A/B the d = 1 gathers: half-warp slot kernel (default) vs staged-record kernel (FEA_GATHER_NO_SLOT1)
+python -m pytest tests -m gpu -x -q > gpurun_out/t.log 2>&1 || { tail -40 gpurun_out/t.log; exit 1; }
+timeout 600 python tools/bench_configs.py --configs 1,3 --runs 5 > gpurun_out/d1_slot1.log 2>&1
+FEA_GATHER_NO_SLOT1=1 timeout 600 python tools/bench_configs.py --configs 1,3 --runs 5 > gpurun_out/d1_rec.log 2>&1
