@@ -421,3 +421,32 @@ def test_degenerate_elements_all_strategies(gpu, orc, mesh, n, d, perm):
         assert plan.assemble(K, strategy="colour").cpu().numpy().tobytes() == want_col.tobytes()
         assert plan.assemble(K, strategy="colour_passes").cpu().numpy().tobytes() == want_col.tobytes()
         assert close(plan.assemble(K, strategy="atomic").cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("mesh,n,d", [("hex8", 3, 3), ("tet4", 2, 2), ("quad4", 4, 2)])
+def test_isolated_rows_and_unaligned_k(gpu, orc, mesh, n, d):
+    """Rows of nodes no element touches (their CSR rows are empty), and an element-matrix buffer
+    that is only 8-byte aligned (the bulk-copy gather needs 16 bytes and hands over to the
+    column-node kernel): both bit-exact against the oracle."""
+    import torch
+    conn, nn = M.make_mesh(mesh, n, "elements")
+    extra = 5  # isolated trailing nodes
+    ed = M.element_dofs(conn, d)
+    P = orc.Pattern.build(conn, nn + extra, d)
+    Kh = orc.fill_k(11, conn.shape[0], ed.shape[1])
+    want = P.assemble_sequential(ed, Kh)
+    with gpu.Plan(ed, (nn + extra) * d, dofs_per_node=d) as plan:
+        rp, _ = plan.csr()
+        assert np.all(np.diff(rp[-extra * d - 1:]) == 0)
+        K = torch.from_numpy(Kh).cuda()
+        assert plan.assemble(K, strategy="sorted").cpu().numpy().tobytes() == want.tobytes()
+        flat = torch.empty(Kh.size + 1, dtype=torch.float64, device="cuda")
+        Ku = flat[1:].view(Kh.shape)
+        Ku.copy_(K)
+        assert Ku.data_ptr() % 16 == 8
+        assert plan.assemble(Ku, strategy="sorted").cpu().numpy().tobytes() == want.tobytes()
+        col, _ = orc.greedy_colouring(conn, nn + extra)
+        plan.set_colouring(col)
+        want_col = P.assemble_coloured(ed, Kh, col)
+        for k in (K, Ku):
+            assert plan.assemble(k, strategy="colour").cpu().numpy().tobytes() == want_col.tobytes()
