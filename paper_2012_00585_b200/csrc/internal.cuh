@@ -98,6 +98,11 @@ struct fea_plan {
     feagpu::DevBuf posA;      // PosT [n_adj*npe] positions, adjacency order (gather route)
     feagpu::DevBuf posE;      // PosT [E*npe*npe] positions, element order (atomic/colour routes; lazy)
     feagpu::DevBuf order;     // int32 [E] atomic-route element order (lazy)
+    // atomic route, common shapes: metadata in visit order (k_atomic_staged; lazy)
+    feagpu::DevBuf at_krow;   // int32 [at_E_pad] K row of the i-th visited element
+    feagpu::DevBuf at_rows;   // int64 [at_E_pad*npe] values start << 20 | row length (-1: not owned)
+    feagpu::DevBuf at_pos;    // PosT [at_E_pad*npe*npe] row-relative positions
+    int64_t at_E_pad = 0;     // E rounded up to whole warp steps
     feagpu::DevBuf node_order;  // int32 [n_own] gather traversal order (empty: node id order)
     // d = 1 with a traversal order: the sorted incidences re-laid in traversal order, so the
     // gather reads them sequentially (else: random 128 B line fetches per node)

@@ -1057,6 +1057,160 @@ __global__ void __launch_bounds__(kWarps * 32)
 }
 
 // ---------------------------------------------------------------------------
+// Element-owner atomics, staged (FEA_ATOMIC for the common shapes)
+// ---------------------------------------------------------------------------
+// k_scatter above is bound by latency, not by the reductions: per element a chain of four
+// dependent metadata loads (list -> elem_krow -> conn_k -> nptr), then one dependent position
+// load per entry, with ~4 K loads in flight per lane (ncu: 75 % of stall samples on the REDs'
+// operands, L2 36 % busy). Here the metadata is laid out in visit order at plan time
+// (at_krow / at_rows / at_pos: sequential reads), and a warp streams a "step" of B elements
+// (their K blocks, row words and position bytes) into shared memory with 16-byte cp.async,
+// STAGES - 1 steps ahead, so the K bytes of several elements per warp are in flight while it
+// issues the reductions of the current one. Entry -> slot: row word of the entry's row node
+// (values start << 20 | row length, -1 off-partition) + ki * row length + pos * d + kj.
+// One RED.E.ADD.F64 per entry, lanes on consecutive entries of the row-major block, as
+// assemble_atomic (assembly.hpp:121-126) does one fetch_add per entry.
+#ifndef FEA_AT_STAGES
+#define FEA_AT_STAGES 3
+#endif
+#ifndef FEA_AT_MINB
+#define FEA_AT_MINB 1
+#endif
+#ifndef FEA_AT_K_EVICT_FIRST
+#define FEA_AT_K_EVICT_FIRST 1  // K is read once: keep the L2 for the values being reduced
+#endif
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void cp_async16_hint(void* dst, const void* src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "l"(pol)
+                 : "memory");
+}
+template <int D, int NPE, class PosT>
+struct AtomicShape {
+    static constexpr int M = D * NPE;
+    static constexpr int MM = M * M;
+    static constexpr int B = MM >= 128 ? 1 : 128 / MM;  // elements per warp step
+    static constexpr int KD = B * MM;                    // K doubles per step
+    static constexpr int T = (KD + 31) / 32;             // entries per lane per step
+    static constexpr int RB = B * NPE * 8;               // row-word bytes per step
+    static constexpr int PB = B * NPE * NPE * static_cast<int>(sizeof(PosT));  // position bytes per step
+    static constexpr int STAGE = KD * 8 + RB + ((PB + 15) & ~15);
+    static_assert(MM % 2 == 0 && RB % 16 == 0 && PB % 16 == 0, "16-byte staging pieces");
+};
+
+template <int D, int NPE, class PosT, int STAGES>
+__global__ void __launch_bounds__(kWarps * 32, FEA_AT_MINB)
+    k_atomic_staged(const double* __restrict__ K, const int32_t* __restrict__ at_krow,
+                    const int64_t* __restrict__ at_rows, const PosT* __restrict__ at_pos, int64_t n_steps,
+                    double* __restrict__ values) {
+    using S = AtomicShape<D, NPE, PosT>;
+    constexpr int M = S::M, MM = S::MM, B = S::B, KD = S::KD;
+    extern __shared__ __align__(16) unsigned char smem_at[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    unsigned char* wbuf = smem_at + static_cast<size_t>(warp) * STAGES * S::STAGE;
+    const int64_t W = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int64_t s0 = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+    const uint64_t kpol = FEA_AT_K_EVICT_FIRST ? l2_policy_evict_first() : 0;
+
+    // lane bb < B holds the K row of element bb of a step
+    auto krow_of = [&](int64_t st) -> int32_t {
+        return (st < n_steps && lane < B) ? at_krow[st * B + lane] : 0;
+    };
+    auto issue = [&](int stage, int64_t st, int32_t kr) {
+        if (st < n_steps) {
+            unsigned char* sb = wbuf + stage * S::STAGE;
+            double* kd = reinterpret_cast<double*>(sb);
+#pragma unroll
+            for (int base = 0; base < KD / 2; base += 32) {  // warp-uniform trips (shuffles)
+                const int pc = base + lane;
+                const int bb = min(pc / (MM / 2), B - 1);
+                const int32_t r = __shfl_sync(0xffffffffu, kr, bb);
+                const double* src = K + static_cast<int64_t>(r) * MM + 2 * (pc - bb * (MM / 2));
+                if (pc < KD / 2) {
+                    if (FEA_AT_K_EVICT_FIRST) cp_async16_hint(kd + 2 * pc, src, kpol);
+                    else cp_async16(kd + 2 * pc, src);
+                }
+            }
+            const unsigned char* rs = reinterpret_cast<const unsigned char*>(at_rows + st * B * NPE);
+            for (int pc = lane; pc < S::RB / 16; pc += 32) cp_async16(sb + KD * 8 + 16 * pc, rs + 16 * pc);
+            const unsigned char* ps = reinterpret_cast<const unsigned char*>(at_pos) + st * S::PB;
+            for (int pc = lane; pc < S::PB / 16; pc += 32) cp_async16(sb + KD * 8 + S::RB + 16 * pc, ps + 16 * pc);
+        }
+        cp_async_commit();
+    };
+
+    // prologue: STAGES - 1 steps in flight
+    int32_t kr_next = 0;
+#pragma unroll
+    for (int k = 0; k < STAGES - 1; ++k) issue(k, s0 + k * W, krow_of(s0 + k * W));
+    kr_next = krow_of(s0 + (STAGES - 1) * W);
+    int stage = 0;
+    for (int64_t st = s0; st < n_steps; st += W) {
+        issue((stage + STAGES - 1) % STAGES, st + (STAGES - 1) * W, kr_next);
+        kr_next = krow_of(st + STAGES * W);
+        asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 1) : "memory");
+        __syncwarp();
+        const unsigned char* sb = wbuf + stage * S::STAGE;
+        const double* kd = reinterpret_cast<const double*>(sb);
+        const int64_t* rows = reinterpret_cast<const int64_t*>(sb + KD * 8);
+        const PosT* pos = reinterpret_cast<const PosT*>(sb + KD * 8 + S::RB);
+#pragma unroll
+        for (int t = 0; t < S::T; ++t) {
+            const int idx = lane + 32 * t;
+            if (KD % 32 != 0 && idx >= KD) break;
+            const int bb = idx / MM, r = idx - bb * MM;
+            const int i = r / M, j = r - (r / M) * M;
+            const int a = i / D, ki = i - a * D, b = j / D, kj = j - b * D;
+            const int64_t w = rows[bb * NPE + a];
+            if (w >= 0) {
+                const int64_t slot = (w >> 20) + static_cast<int64_t>(ki) * (w & 0xfffff) +
+                                     static_cast<int64_t>(pos[(bb * NPE + a) * NPE + b]) * D + kj;
+                atomicAdd(values + slot, kd[idx]);
+            }
+        }
+        __syncwarp();  // this stage is refilled by the next iteration's issue
+        stage = (stage + 1) % STAGES;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// visit-order metadata for k_atomic_staged (padded to whole steps: row words -1, K row 0)
+template <class PosT>
+__global__ void k_atomic_maps(const int32_t* __restrict__ order, const int32_t* __restrict__ elem_krow,
+                              const int32_t* __restrict__ conn_k, const int64_t* __restrict__ nptr,
+                              const PosT* __restrict__ posE, int64_t E, int64_t E_pad, int npe, int d,
+                              int64_t node_begin, int64_t n_own, int32_t* __restrict__ at_krow,
+                              int64_t* __restrict__ at_rows, PosT* __restrict__ at_pos) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E_pad;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i >= E) {
+            at_krow[i] = 0;
+            for (int a = 0; a < npe; ++a) at_rows[i * npe + a] = -1;
+            for (int q = 0; q < npe * npe; ++q) at_pos[i * npe * npe + q] = 0;
+            continue;
+        }
+        const int32_t le = order[i];
+        const int32_t kr = elem_krow[le];
+        at_krow[i] = kr;
+        for (int a = 0; a < npe; ++a) {
+            const int64_t v = conn_k[static_cast<int64_t>(kr) * npe + a] - node_begin;
+            int64_t w = -1;
+            if (v >= 0 && v < n_own) {
+                const int64_t c0 = nptr[v];
+                w = ((static_cast<int64_t>(d) * d * c0) << 20) | (static_cast<int64_t>(d) * (nptr[v + 1] - c0));
+            }
+            at_rows[i * npe + a] = w;
+        }
+        for (int q = 0; q < npe * npe; ++q) at_pos[i * npe * npe + q] = posE[static_cast<int64_t>(le) * npe * npe + q];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Element-order maps for the element-owner routes (built lazily)
 // ---------------------------------------------------------------------------
 template <class PosT>
@@ -1394,6 +1548,41 @@ void scatter(fea_plan* p, const double* K, const int32_t* list, int64_t n_list, 
     else if (mm <= 8) run_scatter<8, PosT, ATOMIC>(p, K, list, n_list, values, s);
     else if (mm <= 16) run_scatter<16, PosT, ATOMIC>(p, K, list, n_list, values, s);
     else run_scatter<32, PosT, ATOMIC>(p, K, list, n_list, values, s);
+}
+
+template <int D, int NPE, class PosT>
+void run_atomic_staged(fea_plan* p, const double* K, double* values, cudaStream_t s) {
+    using S = AtomicShape<D, NPE, PosT>;
+    constexpr int STAGES = FEA_AT_STAGES;
+    const int64_t n_steps = p->at_E_pad / S::B;
+    if (n_steps == 0) return;
+    const size_t smem = static_cast<size_t>(kWarps) * STAGES * S::STAGE;
+    auto kern = k_atomic_staged<D, NPE, PosT, STAGES>;
+    if (smem > 48 * 1024)
+        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0, sms = 0;
+    FEA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem));
+    FEA_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+    const int64_t blocks = std::min<int64_t>((n_steps + kWarps - 1) / kWarps,
+                                             static_cast<int64_t>(sms) * std::max(per_sm, 1));
+    kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
+        K, p->at_krow.as<int32_t>(), p->at_rows.as<int64_t>(), p->at_pos.as<PosT>(), n_steps, values);
+    FEA_CK(cudaGetLastError());
+    p->last_launches += 1;
+}
+
+template <class PosT>
+bool atomic_staged(fea_plan* p, const double* K, double* values, cudaStream_t s) {
+    if (!p->at_krow.p || (reinterpret_cast<uintptr_t>(K) & 15u) != 0) return false;
+    switch (p->d * 16 + p->npe) {
+        case 1 * 16 + 4: run_atomic_staged<1, 4, PosT>(p, K, values, s); return true;
+        case 2 * 16 + 4: run_atomic_staged<2, 4, PosT>(p, K, values, s); return true;
+        case 3 * 16 + 4: run_atomic_staged<3, 4, PosT>(p, K, values, s); return true;
+        case 1 * 16 + 8: run_atomic_staged<1, 8, PosT>(p, K, values, s); return true;
+        case 2 * 16 + 8: run_atomic_staged<2, 8, PosT>(p, K, values, s); return true;
+        case 3 * 16 + 8: run_atomic_staged<3, 8, PosT>(p, K, values, s); return true;
+        default: return false;
+    }
 }
 
 }  // namespace

@@ -1069,7 +1069,7 @@ int64_t metadata_bytes(const fea_plan* p) {
     return static_cast<int64_t>(p->conn_k.bytes + p->elem_id.bytes + p->elem_krow.bytes +
                                 p->adj_ptr.bytes + p->adj.bytes + p->nptr.bytes + p->ncol.bytes +
                                 p->nrun_ptr.bytes + p->posA.bytes + p->posE.bytes +
-                                p->order.bytes + p->colour_elems.bytes + p->adjC.bytes + p->posAC.bytes +
+                                p->order.bytes + p->at_krow.bytes + p->at_rows.bytes + p->at_pos.bytes + p->colour_elems.bytes + p->adjC.bytes + p->posAC.bytes +
                                 p->node_order.bytes + p->trav_ptr.bytes + p->trav_meta.bytes +
                                 p->trav_rec.bytes);
 }

@@ -450,3 +450,32 @@ def test_isolated_rows_and_unaligned_k(gpu, orc, mesh, n, d):
         want_col = P.assemble_coloured(ed, Kh, col)
         for k in (K, Ku):
             assert plan.assemble(k, strategy="colour").cpu().numpy().tobytes() == want_col.tobytes()
+
+
+@pytest.mark.parametrize("mesh,n,d,perm", [c for c in CASES if c[0] in ("quad4", "hex8", "tet4")])
+def test_atomic_staged_vs_legacy(gpu, orc, mesh, n, d, perm, monkeypatch):
+    """The staged atomic kernel (visit-order metadata, cp.async-staged K) and the legacy
+    k_scatter<atomic> (FEA_ATOMIC_LEGACY=1, also the path for a K that is not 16-byte
+    aligned) both match assemble_sequential within the reference tolerance, and agree
+    bitwise with ones K (integer sums are exact in any order)."""
+    import torch
+    conn, nn, ed, n_rows = problem(mesh, n, d, perm)
+    E, m = ed.shape
+    P = orc.Pattern.build(conn, nn, d)
+    Kh = orc.fill_k(42, E, m)
+    want = P.assemble_sequential(ed, Kh)
+    ones_want = P.assemble_sequential(ed, np.ones((E, m, m)))
+    K = torch.from_numpy(Kh).cuda()
+    buf = torch.empty(E * m * m + 1, dtype=torch.float64, device="cuda")
+    K_odd = buf[1:].view(E, m, m)  # 8-byte aligned only: legacy kernel
+    K_odd.copy_(K)
+    for legacy in (False, True):
+        if legacy:
+            monkeypatch.setenv("FEA_ATOMIC_LEGACY", "1")
+        else:
+            monkeypatch.delenv("FEA_ATOMIC_LEGACY", raising=False)
+        with gpu.Plan(ed, n_rows, dofs_per_node=d) as plan:
+            assert close(plan.assemble(K, strategy="atomic").cpu().numpy(), want)
+            assert close(plan.assemble(K_odd, strategy="atomic").cpu().numpy(), want)
+            ones = torch.ones((E, m, m), dtype=torch.float64, device="cuda")
+            assert plan.assemble(ones, strategy="atomic").cpu().numpy().tobytes() == ones_want.tobytes()
