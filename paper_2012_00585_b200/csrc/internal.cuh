@@ -110,6 +110,8 @@ struct fea_plan {
     feagpu::DevBuf trav_meta;  // int64 [n_own] values start << 20 | row length
     feagpu::DevBuf trav_rec;   // int32 [n_adj*trav_rw] {entry, position words[, pad]}
     int32_t trav_rw = 0;
+    int64_t cn_cta_acc = 0;     // packed accumulator doubles per CTA of k_gather_cn (lazy)
+    int32_t cn_cta_per = 0;
     // colouring
     bool has_colouring = false;
     feagpu::DevBuf colour_elems;           // int32 [E] local elements grouped by colour, ascending id

@@ -508,13 +508,21 @@ __global__ void __launch_bounds__(kWarps * 32, gather_min_blocks<R>())
 #ifndef FEA_CN_MINB
 #define FEA_CN_MINB 6
 #endif
+template <int G, int PF>
+constexpr int cn_min_blocks() {  // warp-wide groups with one row block in flight fit 64 registers
+#ifdef FEA_CN32_MINB
+    return G == 32 ? FEA_CN32_MINB : FEA_CN_MINB;
+#else
+    return G == 32 && PF == 1 ? 8 : FEA_CN_MINB;
+#endif
+}
 template <int G, int D, int PF, class PosT, bool DISTINCT, bool GEN>
-__global__ void __launch_bounds__(kWarps * 32, FEA_CN_MINB)
+__global__ void __launch_bounds__(kWarps * 32, cn_min_blocks<G, PF>())
     k_gather_cn(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
                 const int32_t* __restrict__ adj, const PosT* __restrict__ posA,
                 const int64_t* __restrict__ nptr, const int32_t* __restrict__ order, int64_t n_own,
                 int npe, int pstride, int acc_stride, int pos_stride, int accumulate, GenK gen,
-                double* __restrict__ values) {
+                int64_t cta_acc, double* __restrict__ values) {
     extern __shared__ double sacc[];
     constexpr int GPW = 32 / G;
     constexpr int R = D * D;
@@ -526,10 +534,6 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_CN_MINB)
     const int warp = threadIdx.x >> 5;
     const int grp = warp * GPW + gw;
     const bool col_ok = gl < npe;
-    double* acc = sacc + static_cast<int64_t>(grp) * acc_stride;
-    PosT* spos = reinterpret_cast<PosT*>(sacc + static_cast<int64_t>(kWarps) * GPW * acc_stride) +
-                 static_cast<int64_t>(grp) * pos_stride;
-
     const int64_t vi = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * GPW + gw;
     const int64_t v = (order != nullptr && vi < n_own) ? order[vi] : vi;
     int64_t b0 = 0, vb = 0;
@@ -542,15 +546,26 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_CN_MINB)
         block = D * rowlen;
         vb = static_cast<int64_t>(D) * D * c0;
     }
-    const int32_t my_ent = gl < n ? adj[b0 + gl] : 0;
-    for (int q = gl; q < n * npe; q += G) {
-        const int k = q / npe;
-        spos[q] = posA[(b0 + k) * pstride + (q - k * npe)];
+    // accumulators: acc_stride doubles per group, or (cta_acc > 0) packed — group g of the CTA
+    // starts after the blocks (+1 bank stagger) of groups 0..g-1, cta_acc = the largest CTA total
+    // (node rows differ in length, e.g. 125 / 75 / 45 / 27 column nodes on hex27)
+    int64_t acc_off = static_cast<int64_t>(grp) * acc_stride;
+    if (cta_acc > 0) {
+        acc_off = 0;
+        const int64_t vi0 = static_cast<int64_t>(blockIdx.x) * kWarps * GPW;
+        for (int g = 0; g < grp; ++g) {
+            if (vi0 + g >= n_own) break;
+            const int64_t u = order != nullptr ? order[vi0 + g] : vi0 + g;
+            acc_off += static_cast<int64_t>(D) * D * (nptr[u + 1] - nptr[u]) + 1;
+        }
     }
-    for (int i = gl; i < block; i += G) acc[i] = accumulate ? values[vb + i] : 0.0;
-    const int n_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
-    __syncwarp();
-
+    double* acc = sacc + acc_off;
+    PosT* spos = reinterpret_cast<PosT*>(sacc + (cta_acc > 0 ? static_cast<int64_t>(cta_acc)
+                                                              : static_cast<int64_t>(kWarps) * GPW * acc_stride)) +
+                 static_cast<int64_t>(grp) * pos_stride;
+    const int32_t my_ent = gl < n ? adj[b0 + gl] : 0;
+    // the first row blocks' K loads depend only on the incidence list: issue them before
+    // the position/accumulator set-up so their latency overlaps it
     double kv[PF][R];
     auto load = [&](int p, int k) {
         const int32_t e0 = __shfl_sync(0xffffffffu, my_ent, (gw * G + (k & (G - 1))) & 31);
@@ -575,6 +590,31 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_CN_MINB)
     };
 #pragma unroll
     for (int p = 0; p < PF; ++p) load(p, p);
+    {   // the node's position rows, copied as 4-byte words in posA's layout (pstride per
+        // incidence): all loads in flight before the stores (a byte-wise copy loop was a chain
+        // of dependent load -> store round trips, 12 % of the stall samples on hex27)
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(posA + b0 * pstride);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(spos);
+        const int words = n * pstride * static_cast<int>(sizeof(PosT)) / 4;
+        constexpr int U = 4;
+        for (int q0 = 0; q0 < words; q0 += U * G) {
+            uint32_t w[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int q = q0 + u * G + gl;
+                w[u] = q < words ? src[q] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int q = q0 + u * G + gl;
+                if (q < words) dst[q] = w[u];
+            }
+        }
+    }
+    for (int i = gl; i < block; i += G) acc[i] = accumulate ? values[vb + i] : 0.0;
+    const int n_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
+    __syncwarp();
+
 
     for (int k0 = 0; k0 < n_max; k0 += PF) {
 #pragma unroll
@@ -584,7 +624,7 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_CN_MINB)
                 // a repeated node: two lanes (columns) share slots; fold lane by lane in column order
                 for (int l = 0; l < G; ++l) {
                     if (k < n && col_ok && gl == l) {
-                        const int base = static_cast<int>(spos[k * npe + gl]) * D;
+                        const int base = static_cast<int>(spos[k * pstride + gl]) * D;
 #pragma unroll
                         for (int ki = 0; ki < D; ++ki)
 #pragma unroll
@@ -593,7 +633,7 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_CN_MINB)
                     __syncwarp();
                 }
             } else if (k < n && col_ok) {
-                const int base = static_cast<int>(spos[k * npe + gl]) * D;
+                const int base = static_cast<int>(spos[k * pstride + gl]) * D;
                 FEA_DCHECK(base + (D - 1) * rowlen + D - 1 < block);
                 {
                     double a[R];
@@ -1332,7 +1372,7 @@ void run_gather_node(fea_plan* p, const Incidences& in, const double* K, double*
                      cudaStream_t s) {
     constexpr int GPW = 32 / G;
     const int acc_stride = p->d * p->d * p->max_cnt + 1;  // +1 staggers groups across banks
-    const int pos_stride = static_cast<int>((std::max<int64_t>(p->max_adj, 1) * p->npe + 7) & ~int64_t(7));
+    const int pos_stride = static_cast<int>((std::max<int64_t>(p->max_adj, 1) * p->pstride + 7) & ~int64_t(7));
     size_t smem = static_cast<size_t>(kWarps) * GPW *
                   (acc_stride * sizeof(double) + pos_stride * sizeof(PosT));
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID,
@@ -1403,14 +1443,53 @@ bool slot_applies(const fea_plan* p) {
 #ifndef FEA_CN_PF8
 #define FEA_CN_PF8 2
 #endif
+// largest per-CTA sum of node blocks (+1 stagger each) over CTAs of `per_cta` consecutive
+// traversal nodes: the packed accumulator size of k_gather_cn
+__global__ void k_cta_acc_max(const int32_t* __restrict__ order, const int64_t* __restrict__ nptr,
+                              int64_t n_own, int dd, int per_cta, unsigned long long* out) {
+    const int64_t n_cta = (n_own + per_cta - 1) / per_cta;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_cta;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long sum = 0;
+        for (int g = 0; g < per_cta; ++g) {
+            const int64_t t = c * per_cta + g;
+            if (t >= n_own) break;
+            const int64_t u = order != nullptr ? order[t] : t;
+            sum += static_cast<unsigned long long>(dd * (nptr[u + 1] - nptr[u]) + 1);
+        }
+        atomicMax(out, sum);
+    }
+}
+
+int64_t cn_cta_acc(fea_plan* p, int per_cta, cudaStream_t s) {
+    if (std::getenv("FEA_CN_UNPACKED")) return static_cast<int64_t>(per_cta) * (p->d * p->d * p->max_cnt + 1);
+    if (p->cn_cta_acc > 0 && p->cn_cta_per == per_cta) return p->cn_cta_acc;
+    DevBuf out;
+    out.alloc(8);
+    FEA_CK(cudaMemsetAsync(out.p, 0, 8, s));
+    if (p->n_own > 0) {
+        k_cta_acc_max<<<grid_for((p->n_own + per_cta - 1) / per_cta, 256), 256, 0, s>>>(
+            p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->nptr.as<int64_t>(), p->n_own,
+            p->d * p->d, per_cta, out.as<unsigned long long>());
+        FEA_CK(cudaGetLastError());
+    }
+    unsigned long long v = 0;
+    FEA_CK(cudaMemcpyAsync(&v, out.p, 8, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaStreamSynchronize(s));
+    p->cn_cta_acc = std::max<int64_t>(static_cast<int64_t>(v), 1);
+    p->cn_cta_per = per_cta;
+    return p->cn_cta_acc;
+}
+
 template <int G, int D, int PF, class PosT>
 void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
                    cudaStream_t s) {
     constexpr int GPW = 32 / G;
     const int acc_stride = p->d * p->d * p->max_cnt + 1;  // +1 staggers groups across banks (swept: 1-2 best)
-    const int pos_stride = static_cast<int>((std::max<int64_t>(p->max_adj, 1) * p->npe + 7) & ~int64_t(7));
-    const size_t smem = static_cast<size_t>(kWarps) * GPW *
-                        (acc_stride * sizeof(double) + pos_stride * sizeof(PosT));
+    const int pos_stride = static_cast<int>((std::max<int64_t>(p->max_adj, 1) * p->pstride + 7) & ~int64_t(7));
+    const int64_t cta_acc = cn_cta_acc(p, kWarps * GPW, s);
+    const size_t smem = static_cast<size_t>(cta_acc) * sizeof(double) +
+                        static_cast<size_t>(kWarps) * GPW * pos_stride * sizeof(PosT);
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
     auto kern = p->gen_on ? (p->dup_nodes ? k_gather_cn<G, D, PF, PosT, false, true>
                                           : k_gather_cn<G, D, PF, PosT, true, true>)
@@ -1423,7 +1502,7 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
         K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const PosT*>(in.posA), p->nptr.as<int64_t>(),
         p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, p->npe, p->pstride, acc_stride,
-        pos_stride, accumulate ? 1 : 0, gen_of(p), values);
+        pos_stride, accumulate ? 1 : 0, gen_of(p), cta_acc, values);
     FEA_CK(cudaGetLastError());
     p->last_launches += 1;
 }
@@ -1502,7 +1581,10 @@ void gather(fea_plan* p, const Incidences& in, const double* K, double* values, 
             case 83: return run_gather_cn<8, 3, FEA_CN_PF8, PosT>(p, in, K, values, accumulate, s);
             case 84: return run_gather_cn<8, 4, 2, PosT>(p, in, K, values, accumulate, s);
             case 163: return run_gather_cn<16, 3, 2, PosT>(p, in, K, values, accumulate, s);
-            case 323: return run_gather_cn<32, 3, 2, PosT>(p, in, K, values, accumulate, s);
+#ifndef FEA_CN_PF32
+#define FEA_CN_PF32 2  // swept on hex27 (cfg4), packed accumulators: PF 1 (64 regs, 7 CTAs/SM) 1.99 ms, PF 2 (80 regs, 6) 1.95, PF 2 at 72 regs 2.06, PF 3 spills
+#endif
+            case 323: return run_gather_cn<32, 3, FEA_CN_PF32, PosT>(p, in, K, values, accumulate, s);
             default: break;
         }
     }
