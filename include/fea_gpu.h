@@ -233,6 +233,21 @@ FEA_API fea_status fea_spmv_crac(const int64_t* row_ptr, const int64_t* col_alig
 FEA_API fea_status fea_plan_spmv(const fea_plan* plan, const double* values, const double* x, double* y,
                                  void* stream);
 
+/*
+ * Peer memory for the fused row-partitioned assembly + gather (no reference
+ * counterpart — the reference is shared-memory only). The root exports its global
+ * values buffer, every rank maps it and fea_assemble()s its owned row block straight into it at
+ * the block's global offset: the kernel's value stores go over NVLink/NVSwitch as they are
+ * produced, so the gather overlaps the assembly instead of following it.
+ *  fea_ipc_export: CUDA IPC handle (64 bytes) of the allocation holding dev_ptr, and dev_ptr's
+ *                  byte offset inside it (works for sub-allocations of caching allocators)
+ *  fea_ipc_open:   map an exported allocation into this process on `device` (peer access
+ *                  enabled lazily); *base is the allocation start; fea_ipc_close unmaps it
+ */
+FEA_API fea_status fea_ipc_export(const void* dev_ptr, void* handle64, int64_t* offset_bytes);
+FEA_API fea_status fea_ipc_open(const void* handle64, int device, void** base);
+FEA_API fea_status fea_ipc_close(void* base);
+
 #ifdef __cplusplus
 }
 #endif

@@ -181,6 +181,15 @@ class Plan:
                                       _stream_ptr(stream)))
         return values
 
+    def assemble_into(self, K, values_ptr: int, strategy: str = "sorted", accumulate: bool = False,
+                      stream=None):
+        """Assemble into a raw device address (e.g. this rank's row block inside the root's
+        global values buffer, mapped with dist.PeerValues): the kernel's stores go to wherever
+        the pointer lives, peer memory over NVLink included."""
+        flags = (N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE) | _EXTRA_FLAGS.get(strategy, 0)
+        _check(self._lib.fea_assemble(self._h, _ptr(K), STRATEGIES[strategy], c_void_p(values_ptr), flags,
+                                      _stream_ptr(stream)))
+
     def assemble_seeded(self, seed: int, values=None, strategy: str = "sorted", accumulate: bool = False,
                         stream=None):
         """Fused supplier: assemble the seeded element matrices generated inside the kernel."""

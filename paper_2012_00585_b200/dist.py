@@ -68,6 +68,65 @@ def gather_row_blocks(values_local, root: int = 0, group=None):
     return torch.cat([o[:s] for o, s in zip(out, sizes)])
 
 
+class PeerValues:
+    """Fused assembly + gather over peer memory: the root allocates the GLOBAL values array,
+    exports it (CUDA IPC, fea_ipc_export) and every rank maps it (fea_ipc_open); rank r's row
+    block starts at the sum of the NNZ of the ranks before it (contiguous ownership = global row
+    order). Each rank then assembles straight into `ptr` (Plan.assemble_into): the numeric
+    kernel's value stores travel over NVLink/NVSwitch while the block is assembled, instead of
+    an NCCL gather after the kernel. After every rank's stream has finished and a barrier,
+    `full` on the root holds the global values. Collective: every rank constructs it.
+    """
+
+    def __init__(self, local_nnz: int, device, root: int = 0, group=None):
+        import ctypes
+        from ctypes import byref, c_int64, c_void_p
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _native as N
+        from .assembly import _check
+        self._lib = N.lib()
+        self.rank = dist.get_rank(group)
+        world = dist.get_world_size(group)
+        sizes = [None] * world
+        dist.all_gather_object(sizes, int(local_nnz), group=group)
+        self.offset = int(sum(sizes[: self.rank]))
+        self.total = int(sum(sizes))
+        self.full = None
+        self._base = None
+        obj = [None]
+        if self.rank == root:
+            self.full = torch.zeros(max(self.total, 1), dtype=torch.float64, device=device)
+            h = ctypes.create_string_buffer(64)
+            off = c_int64()
+            _check(self._lib.fea_ipc_export(c_void_p(self.full.data_ptr()), h, byref(off)))
+            obj = [(h.raw, off.value)]
+        dist.broadcast_object_list(obj, src=root, group=group)
+        if self.rank == root:
+            base = self.full.data_ptr()
+        else:
+            handle, off = obj[0]
+            b = c_void_p()
+            _check(self._lib.fea_ipc_open(ctypes.create_string_buffer(handle, 64), int(torch.device(device).index or 0),
+                                          byref(b)))
+            self._base = b
+            base = b.value + off
+        self.ptr = base + 8 * self.offset  # this rank's row block
+
+    def close(self) -> None:
+        if self._base is not None:
+            self._lib.fea_ipc_close(self._base)
+            self._base = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def _gather_1d(t, root, group):
     """Gather a 1-D tensor of any length from every rank to `root` (rank order)."""
     return gather_row_blocks(t, root=root, group=group)

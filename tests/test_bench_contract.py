@@ -55,3 +55,5 @@ def test_two_rank_partitioned_bench_matches_single_gpu(gpu):
     d = run(["--gpus", "2", "--steps", "2", "--warmup", "3", "--gather", "--check", "--no-e2e"],
             env={"FEA_BENCH_BACKEND": "gloo", "MASTER_PORT": "29541"})
     assert d["n_gpus"] == 2 and d["gather"]["bitwise_equal_to_single_gpu"] is True
+    # the fused path (each rank assembles into rank 0's buffer through a CUDA IPC mapping)
+    assert d["gather"]["fused_assembly_into_root"]["equal_to_nccl_gather"] is True
