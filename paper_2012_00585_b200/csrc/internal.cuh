@@ -109,6 +109,7 @@ struct fea_plan {
     feagpu::DevBuf trav_ptr;   // int64 [n_own+1] record offsets per traversal position
     feagpu::DevBuf trav_meta;  // int64 [n_own] values start << 20 | row length
     feagpu::DevBuf trav_rec;   // int32 [n_adj*trav_rw] {entry, position words[, pad]}
+    feagpu::DevBuf trav_recC;  // the same for the colour-ordered incidences (adjC / posAC)
     int32_t trav_rw = 0;
     int64_t cn_cta_acc = 0;     // packed accumulator doubles per CTA of k_gather_cn (lazy)
     int32_t cn_cta_per = 0;

@@ -1534,14 +1534,15 @@ void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* v
     const int64_t per_cta = static_cast<int64_t>(kWarps) * GPW;
     const int64_t blocks = (p->n_own + per_cta - 1) / per_cta;
     if (blocks == 0) return;
-    // traversal-ordered records exist for the sorted incidences only (not the colour order)
-    const bool trav = p->trav_rec.p != nullptr && in.adj == p->adj.as<int32_t>();
+    // traversal-ordered records: sorted incidences (trav_rec) or colour-ordered ones (trav_recC)
+    const DevBuf& recs = in.adj == p->adj.as<int32_t>() ? p->trav_rec : p->trav_recC;
+    const bool trav = recs.p != nullptr && (in.adj == p->adj.as<int32_t>() || in.adj == p->adjC.as<int32_t>());
     FEA_REQUIRE(!trav || p->trav_rw == rw, FEA_ERR_INVALID, "traversal record width mismatch");
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
         K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const PosT*>(in.posA), p->nptr.as<int64_t>(),
         p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, p->npe, p->pstride, cap,
         rec_stride, acc_stride, accumulate ? 1 : 0, p->m * 8 < 128 ? 1 : 0, trav ? p->trav_ptr.as<int64_t>() : nullptr,
-        trav ? p->trav_meta.as<int64_t>() : nullptr, trav ? p->trav_rec.as<int32_t>() : nullptr, gen_of(p), values);
+        trav ? p->trav_meta.as<int64_t>() : nullptr, trav ? recs.as<int32_t>() : nullptr, gen_of(p), values);
     FEA_CK(cudaGetLastError());
     p->last_launches += 1;
 }

@@ -1060,6 +1060,19 @@ void build_colour_incidences(fea_plan* p, const std::vector<int32_t>& colour_of_
                                                           p->posA.as<unsigned char>(), p->adjC.as<int32_t>(),
                                                           p->posAC.as<unsigned char>());
     FEA_CK(cudaGetLastError());
+    // d = 1 with traversal records: the colour-ordered incidences get their own records (same
+    // per-node counts and offsets, trav_ptr / trav_meta), so FEA_DET_COLOUR reads them
+    // sequentially like the sorted route
+    p->trav_recC.reset();
+    if (p->trav_rec.p) {
+        const int pw = p->pstride * p->pos_bytes / 4;
+        p->trav_recC.alloc(std::max<int64_t>(n, 1) * p->trav_rw * 4);
+        k_trav_records<<<grid_for(p->n_own * 32, 256), 256, 0, s>>>(
+            p->node_order.as<int32_t>(), p->adj_ptr.as<int64_t>(), p->adjC.as<int32_t>(),
+            static_cast<const uint32_t*>(p->posAC.p), pw, p->trav_rw, p->trav_ptr.as<int64_t>(), p->n_own,
+            p->trav_recC.as<int32_t>());
+        FEA_CK(cudaGetLastError());
+    }
     FEA_CK(cudaStreamSynchronize(s));
 }
 
@@ -1071,7 +1084,7 @@ int64_t metadata_bytes(const fea_plan* p) {
                                 p->nrun_ptr.bytes + p->posA.bytes + p->posE.bytes +
                                 p->order.bytes + p->at_krow.bytes + p->at_rows.bytes + p->at_pos.bytes + p->colour_elems.bytes + p->adjC.bytes + p->posAC.bytes +
                                 p->node_order.bytes + p->trav_ptr.bytes + p->trav_meta.bytes +
-                                p->trav_rec.bytes);
+                                p->trav_rec.bytes + p->trav_recC.bytes);
 }
 
 }  // namespace feagpu
