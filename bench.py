@@ -284,7 +284,7 @@ def run_ours(args):
     peak, peak_src = measured_peak_gbs()
     achieved = min_bytes / (my_ms * 1e-3) / 1e9
     kernel_name = {"sorted": "k_gather_slot<3,8> (warp = node, lane = slot, register accumulators)",
-                   "atomic": "k_scatter<32,u8,atomic>",
+                   "atomic": "k_atomic_staged<3,8,u8> (visit-order metadata, cp.async-staged K, RED.E.ADD.F64)",
                    "colour": "k_gather_slot<3,8> (colour-ordered incidences)",
                    "colour_passes": "k_scatter<32,u8,plain> x n_colours"}[args.strategy]
     traffic = profiled_traffic(f"cfg2/{args.strategy}") if N == 1 else None
