@@ -84,27 +84,29 @@ void ensure_element_maps(fea_plan* p, cudaStream_t s) {
 // Visit-order metadata of k_atomic_staged (shapes d <= 3, npe in {4, 8}); other shapes, and
 // FEA_ATOMIC_LEGACY=1 (A/B), keep k_scatter<atomic>.
 void build_atomic_maps(fea_plan* p, cudaStream_t s) {
-    const bool shape = p->d >= 1 && p->d <= 3 && (p->npe == 4 || p->npe == 8);
+    const bool shape = (p->d >= 1 && p->d <= 3 && (p->npe == 4 || p->npe == 8)) ||
+                       ((p->d == 1 || p->d == 3) && p->npe == 27);  // k_atomic_staged / k_atomic_cta
     if (!shape || p->E == 0 || std::getenv("FEA_ATOMIC_LEGACY") ||
         static_cast<int64_t>(p->d) * p->max_cnt >= (1 << 20))
         return;
     const int mm = p->m * p->m;
-    const int B = mm >= 128 ? 1 : 128 / mm;  // AtomicShape<>::B
+    const int B = mm >= 128 ? 1 : 128 / mm;  // AtomicShape<>::B (k_atomic_cta: 1)
     p->at_E_pad = (p->E + B - 1) / B * B;
-    const int64_t np2 = static_cast<int64_t>(p->npe) * p->npe;
+    // position rows padded to 16-byte multiples (whole cp.async pieces)
+    const int pstr = ((p->npe * p->npe * p->pos_bytes + 15) & ~15) / p->pos_bytes;
     p->at_krow.alloc(p->at_E_pad * 4);
     p->at_rows.alloc(p->at_E_pad * p->npe * 8);
-    p->at_pos.alloc(p->at_E_pad * np2 * p->pos_bytes);
+    p->at_pos.alloc(p->at_E_pad * pstr * p->pos_bytes);
     const unsigned g = grid_for(p->at_E_pad, 256);
     if (p->pos_bytes == 1)
         k_atomic_maps<uint8_t><<<g, 256, 0, s>>>(
             p->order.as<int32_t>(), p->elem_krow.as<int32_t>(), p->conn_k.as<int32_t>(), p->nptr.as<int64_t>(),
-            p->posE.as<uint8_t>(), p->E, p->at_E_pad, p->npe, p->d, p->node_begin, p->n_own,
+            p->posE.as<uint8_t>(), p->E, p->at_E_pad, p->npe, p->d, p->node_begin, p->n_own, pstr,
             p->at_krow.as<int32_t>(), p->at_rows.as<int64_t>(), p->at_pos.as<uint8_t>());
     else
         k_atomic_maps<uint16_t><<<g, 256, 0, s>>>(
             p->order.as<int32_t>(), p->elem_krow.as<int32_t>(), p->conn_k.as<int32_t>(), p->nptr.as<int64_t>(),
-            p->posE.as<uint16_t>(), p->E, p->at_E_pad, p->npe, p->d, p->node_begin, p->n_own,
+            p->posE.as<uint16_t>(), p->E, p->at_E_pad, p->npe, p->d, p->node_begin, p->n_own, pstr,
             p->at_krow.as<int32_t>(), p->at_rows.as<int64_t>(), p->at_pos.as<uint16_t>());
     FEA_CK(cudaGetLastError());
     FEA_CK(cudaStreamSynchronize(s));

@@ -452,7 +452,7 @@ def test_isolated_rows_and_unaligned_k(gpu, orc, mesh, n, d):
             assert plan.assemble(k, strategy="colour").cpu().numpy().tobytes() == want_col.tobytes()
 
 
-@pytest.mark.parametrize("mesh,n,d,perm", [c for c in CASES if c[0] in ("quad4", "hex8", "tet4")])
+@pytest.mark.parametrize("mesh,n,d,perm", CASES)
 def test_atomic_staged_vs_legacy(gpu, orc, mesh, n, d, perm, monkeypatch):
     """The staged atomic kernel (visit-order metadata, cp.async-staged K) and the legacy
     k_scatter<atomic> (FEA_ATOMIC_LEGACY=1, also the path for a K that is not 16-byte
