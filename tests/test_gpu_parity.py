@@ -479,3 +479,40 @@ def test_atomic_staged_vs_legacy(gpu, orc, mesh, n, d, perm, monkeypatch):
             assert close(plan.assemble(K_odd, strategy="atomic").cpu().numpy(), want)
             ones = torch.ones((E, m, m), dtype=torch.float64, device="cuda")
             assert plan.assemble(ones, strategy="atomic").cpu().numpy().tobytes() == ones_want.tobytes()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_unstructured_meshes(gpu, orc, seed):
+    """acceptance.cpp:245-294 (C9, random meshes vs the oracle), on the GPU: random element
+    lists over a random node pool — element sizes npe in {3, 4, 6, 8, 10, 20}, d in 1..5,
+    random node numbering and element order — so every kernel family and the generic shapes
+    (k_gather_node / k_gather_stream / k_scatter) are exercised. Patterns and CRAC arrays
+    bit-exact, sorted and colour routes bit-exact, atomics within the reference tolerance."""
+    import torch
+    rng = np.random.default_rng(1000 + seed)
+    npe = int(rng.choice([3, 4, 6, 8, 10, 20]))
+    d = int(rng.integers(1, 6))
+    nn = int(rng.integers(npe + 2, 200))
+    E = int(rng.integers(1, 300))
+    # distinct nodes per element, drawn from a local window so rows overlap like a real mesh
+    conn = np.empty((E, npe), np.int64)
+    for e in range(E):
+        lo = int(rng.integers(0, max(1, nn - 3 * npe)))
+        conn[e] = lo + rng.choice(min(3 * npe, nn - lo), size=npe, replace=False)
+    ed = M.element_dofs(conn, d)
+    P = orc.Pattern.build(conn, nn, d)
+    rp, cs = P.arrays()
+    Kh = orc.fill_k(seed, E, npe * d)
+    want = P.assemble_sequential(ed, Kh)
+    col, _ = orc.greedy_colouring(conn, nn)
+    want_col = P.assemble_coloured(ed, Kh, col)
+    K = torch.from_numpy(Kh).cuda()
+    with gpu.Plan(ed, nn * d, dofs_per_node=d) as plan:
+        grp, gcs = plan.csr()
+        assert np.array_equal(grp, rp) and np.array_equal(gcs, cs)
+        for got, exp in zip(plan.crac(), P.crac()):
+            assert np.array_equal(got, exp)
+        assert plan.assemble(K, strategy="sorted").cpu().numpy().tobytes() == want.tobytes()
+        plan.set_colouring(col)
+        assert plan.assemble(K, strategy="colour").cpu().numpy().tobytes() == want_col.tobytes()
+        assert close(plan.assemble(K, strategy="atomic").cpu().numpy(), want)
