@@ -805,6 +805,9 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_D1_MINB)
 #ifndef FEA_SLOT_TMA
 #define FEA_SLOT_TMA 1
 #endif
+#ifndef FEA_SLOT_BRANCHLESS
+#define FEA_SLOT_BRANCHLESS 1  // cfg2: 0.310 -> 0.278 ms (same bits)
+#endif
 #ifndef FEA_SLOT_MINB
 #define FEA_SLOT_MINB 6  // swept 4 (95 regs) 0.318 ms, 6 0.303, 8 0.305 on cfg2
 #endif
@@ -838,6 +841,19 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_SLOT_MINB)
         int64_t a0;
         int n;
     };
+#if FEA_SLOT_BRANCHLESS
+    // branch-free prefetch (clamped index, result masked): the loads' consumers are not pinned
+    // right behind them by a branch join
+    auto ptr_of = [&](int64_t t) -> Ptr {
+        const bool ok = t < n_own;
+        const int64_t tc = ok ? t : n_own - 1;
+        const int64_t v = order != nullptr ? order[tc] : tc;
+        Ptr P;
+        P.a0 = adj_ptr[v];
+        P.n = ok ? static_cast<int>(adj_ptr[v + 1] - P.a0) : 0;
+        return P;
+    };
+#else
     auto ptr_of = [&](int64_t t) -> Ptr {
         Ptr P{0, 0};
         if (t < n_own) {
@@ -847,6 +863,7 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_SLOT_MINB)
         }
         return P;
     };
+#endif
     struct Rec {
         int32_t ent;       // lane k: entry of incidence k
         uint32_t pw[PW];   // lane k: position words of incidence k
@@ -861,11 +878,22 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_SLOT_MINB)
         R.n = P.n;
         R.c0 = 0;
         R.cnt = 0;
+#if FEA_SLOT_BRANCHLESS
+        {
+            const bool ok = t < n_own;
+            const int64_t tc = ok ? t : n_own - 1;
+            const int64_t v = order != nullptr ? order[tc] : tc;
+            const int64_t c0 = nptr[v];
+            R.c0 = ok ? c0 : 0;
+            R.cnt = ok ? static_cast<int>(nptr[v + 1] - c0) : 0;
+        }
+#else
         if (t < n_own) {
             const int64_t v = order != nullptr ? order[t] : t;
             R.c0 = nptr[v];
             R.cnt = static_cast<int>(nptr[v + 1] - R.c0);
         }
+#endif
         if (lane < P.n) {
             R.ent = adj[P.a0 + lane];
             const uint32_t* src = reinterpret_cast<const uint32_t*>(posA) + (P.a0 + lane) * PW;
