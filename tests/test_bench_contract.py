@@ -57,3 +57,20 @@ def test_two_rank_partitioned_bench_matches_single_gpu(gpu):
     assert d["n_gpus"] == 2 and d["gather"]["bitwise_equal_to_single_gpu"] is True
     # the fused path (each rank assembles into rank 0's buffer through a CUDA IPC mapping)
     assert d["gather"]["fused_assembly_into_root"]["equal_to_nccl_gather"] is True
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_config5_row_partition_tool_two_ranks(gpu):
+    """tools/cfg5_ranks.py (BASELINE config 5 as a row-partitioned run) at reduced size, 2 ranks
+    over gloo sharing the GPU: the fused assembly into rank 0's buffer equals a single-plan
+    assembly of the whole mesh bit for bit."""
+    e = dict(os.environ, FEA_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29543",
+                        str(ROOT / "tools" / "cfg5_ranks.py"), "--size", "12", "--runs", "1", "--gather", "--check"],
+                       capture_output=True, text=True, timeout=600, env=e, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["ranks"] == 2 and d["gathered_bitwise_equal_to_single_plan"] is True
+    assert d["redundant_element_fraction"] > 0
