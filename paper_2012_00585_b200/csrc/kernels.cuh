@@ -796,7 +796,7 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_D1_MINB)
 // 2gl, 2gl+1 of the incidence's K row and folds both into the node's shared accumulator, so
 // per warp instruction 16 nodes advance (8 in k_gather_d1) at half the instructions per entry
 // (cfg3 fused: 0.89 -> 0.52 ms). With a materialized K this form measured slower (0.93 vs
-// 0.64 ms: 9 CTAs/SM, shared-memory bound), so K loads use k_gather_d1r. Distinct element
+// 0.64 ms: 9 CTAs/SM, shared-memory bound), so K loads use k_gather_d1g. Distinct element
 // nodes only (a lane's two columns are distinct slots); per-slot fold order unchanged
 // (ascending element id from the start value): same bits as k_gather_d1.
 #ifndef FEA_D1V_MINB
@@ -871,35 +871,28 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_D1V_MINB)
     for (int i = gl; i < rl; i += G) __stcs(values + vb + i, acc[i]);
 }
 
-// Ring form of k_gather_d1v (materialized K): the K rows of a node's incidences are copied
-// into a per-group shared-memory ring of R rows by 16-byte cp.async.cg (L2 only, no
-// register destinations), lane gl copying exactly the half row it later folds, so a lane
-// waits only on its own copy groups (cp.async.wait_group R-1) and there is no cross-lane
-// hand-off beyond the per-step __syncwarp the shared accumulator already needs. R rows in
-// flight per group without registers: the register-destination kernels above are capped by
-// the register file at ~46 KB of loads in flight per SM, about half of what HBM latency
-// needs. Same fold order, same bits.
-template <int R>
+// Direct-record form of k_gather_d1 (npe = 4, traversal records, materialized K): no record
+// staging in shared memory (which capped residency at 12-13 CTAs/SM and cost a cp.async round
+// trip per node); each lane reads the group's records straight from global memory through the
+// read-only path (the 4 lanes of a group read the same 8 bytes; ld.global.nc, L1-cached: the
+// streaming .cs form measured 0.60 vs 0.52 ms in tools/gather_probe_d1.py), U at a time, then
+// the U K rows, then folds. Shared memory holds only the accumulators. Same fold order, bits.
+#ifndef FEA_D1G_U
+#define FEA_D1G_U 8  // records + K rows in flight per lane; cfg3: 4 -> 0.620 ms, 8 -> 0.614
+#endif
+template <int U>
 __global__ void __launch_bounds__(kWarps * 32)
-    k_gather_d1r(const double* __restrict__ K, int64_t n_own, int cap, int rec_stride, int acc_stride,
-                 int accumulate, const int64_t* __restrict__ tptr, const int64_t* __restrict__ tmeta,
-                 const int32_t* __restrict__ trec, double* __restrict__ values) {
+    k_gather_d1g(const double* __restrict__ K, int64_t n_own, int acc_stride, int accumulate,
+                 const int64_t* __restrict__ tptr, const int64_t* __restrict__ tmeta,
+                 const int2* __restrict__ trec, double* __restrict__ values) {
     extern __shared__ double sacc[];
-    constexpr int G = 2;
+    constexpr int G = 4;
     constexpr int GPW = 32 / G;
-    constexpr int NG = kWarps * GPW;
     const int lane = threadIdx.x & 31;
-    const int gl = lane & 1;
-    const int grp = (threadIdx.x >> 1);
-    // R rows of 4 doubles (32 B) per group; groups 32 B apart mod 128 B so the 16-byte
-    // accesses of a quarter warp (4 groups x 2 lanes) hit distinct banks
-    constexpr int RS = R * 4 + 4;
-    double* ring = sacc + static_cast<int64_t>(grp) * RS;
-    double* acc = sacc + static_cast<int64_t>(NG) * RS + static_cast<int64_t>(grp) * acc_stride;
-    int32_t* rec = reinterpret_cast<int32_t*>(sacc + static_cast<int64_t>(NG) * (RS + acc_stride)) +
-                   static_cast<int64_t>(grp) * rec_stride;
-
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * NG + grp;
+    const int gl = lane & 3;
+    const int grp = threadIdx.x >> 2;
+    double* acc = sacc + static_cast<int64_t>(grp) * acc_stride;
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kWarps * GPW + grp;
     int64_t a0 = 0, vb = 0;
     int n = 0, rl = 0;
     if (t < n_own) {
@@ -909,37 +902,27 @@ __global__ void __launch_bounds__(kWarps * 32)
         vb = mt >> 20;
         rl = static_cast<int>(mt & 0xfffff);
     }
-    FEA_DCHECK(n <= cap);
-    {
-        const int32_t* src = trec + a0 * 2;
-        for (int i = gl; i < n; i += G) cp_async8(rec + 2 * i, src + 2 * i);
-    }
     for (int i = gl; i < rl; i += G) acc[i] = accumulate ? values[vb + i] : 0.0;
-    cp_async_wait_all();
-    __syncwarp();
     const int n_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
-    auto issue = [&](int k) {
-        if (k < n) {
-            const int e = rec[2 * k];
-            cp_async16(ring + (k % R) * 4 + 2 * gl, K + static_cast<int64_t>(e) * 4 + 2 * gl);
-        }
-        cp_async_commit();
-    };
+    const int2* src = trec + a0;
+    for (int k0 = 0; k0 < n_max; k0 += U) {
+        int2 r[U];
+        double kv[U];
 #pragma unroll
-    for (int k = 0; k < R; ++k) issue(k);
-    for (int k = 0; k < n_max; ++k) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(R - 1) : "memory");  // row k landed
-        if (k < n) {
-            const uint32_t q = static_cast<uint32_t>(rec[2 * k + 1]) >> (16 * gl);
-            const int s0 = q & 0xff, s1 = (q >> 8) & 0xff;
-            FEA_DCHECK(s0 < rl && s1 < rl);
-            const double2 kv = *reinterpret_cast<const double2*>(ring + (k % R) * 4 + 2 * gl);
-            const double x0 = acc[s0], x1 = acc[s1];
-            acc[s0] = x0 + kv.x;
-            acc[s1] = x1 + kv.y;
-        }
+        for (int u = 0; u < U; ++u) r[u] = k0 + u < n ? __ldg(src + k0 + u) : make_int2(0, 0);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            kv[u] = k0 + u < n ? __ldcg(K + static_cast<int64_t>(r[u].x) * 4 + gl) : 0.0;
         __syncwarp();
-        issue(k + R);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (k0 + u < n) {
+                const int q = (static_cast<uint32_t>(r[u].y) >> (8 * gl)) & 0xffu;
+                FEA_DCHECK(q < rl);
+                acc[q] += kv[u];
+            }
+            __syncwarp();
+        }
     }
     for (int i = gl; i < rl; i += G) __stcs(values + vb + i, acc[i]);
 }
@@ -1772,42 +1755,6 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
     p->last_launches += 1;
 }
 
-#ifndef FEA_D1_RING
-#define FEA_D1_RING 2  // rows in flight per node group; swept 2/3/4/6/8/12/16 on cfg3
-#endif
-template <int R>
-void launch_d1r(fea_plan* p, const DevBuf& recs, const double* K, double* values, bool accumulate, int cap,
-                int rec_stride, int acc_stride, cudaStream_t s) {
-    constexpr int NG = kWarps * 16;
-    const size_t smem = static_cast<size_t>(NG) *
-                        ((R * 4 + 4 + acc_stride) * sizeof(double) + static_cast<size_t>(rec_stride) * sizeof(int32_t));
-    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
-    if (smem > 48 * 1024)
-        FEA_CK(cudaFuncSetAttribute(k_gather_d1r<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t blocks = (p->n_own + NG - 1) / NG;
-    if (blocks == 0) return;
-    k_gather_d1r<R><<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
-        K, p->n_own, cap, rec_stride, acc_stride, accumulate ? 1 : 0, p->trav_ptr.as<int64_t>(),
-        p->trav_meta.as<int64_t>(), recs.as<int32_t>(), values);
-    FEA_CK(cudaGetLastError());
-    p->last_launches += 1;
-}
-void run_gather_d1r(fea_plan* p, const DevBuf& recs, const double* K, double* values, bool accumulate, int cap,
-                    int rec_stride, int ring, cudaStream_t s) {
-    // ring width R = rows in flight per node group; accumulator stride 3 (mod 16) as k_gather_d1
-    int acc_stride = std::max(p->max_cnt, 1);
-    int acc_mod = 3;
-    if (const char* e = std::getenv("FEA_D1V_ACC_STRIDE_MOD16")) acc_mod = std::atoi(e) & 15;
-    while ((acc_stride & 15) != acc_mod) ++acc_stride;
-    if (ring <= 2) return launch_d1r<2>(p, recs, K, values, accumulate, cap, rec_stride, acc_stride, s);
-    if (ring <= 3) return launch_d1r<3>(p, recs, K, values, accumulate, cap, rec_stride, acc_stride, s);
-    if (ring <= 4) return launch_d1r<4>(p, recs, K, values, accumulate, cap, rec_stride, acc_stride, s);
-    if (ring <= 6) return launch_d1r<6>(p, recs, K, values, accumulate, cap, rec_stride, acc_stride, s);
-    if (ring <= 8) return launch_d1r<8>(p, recs, K, values, accumulate, cap, rec_stride, acc_stride, s);
-    if (ring <= 12) return launch_d1r<12>(p, recs, K, values, accumulate, cap, rec_stride, acc_stride, s);
-    return launch_d1r<16>(p, recs, K, values, accumulate, cap, rec_stride, acc_stride, s);
-}
-
 template <int G, int PF, class PosT>
 void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
                    cudaStream_t s) {
@@ -1839,11 +1786,23 @@ void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* v
     const DevBuf& recs = in.adj == p->adj.as<int32_t>() ? p->trav_rec : p->trav_recC;
     const bool trav = recs.p != nullptr && (in.adj == p->adj.as<int32_t>() || in.adj == p->adjC.as<int32_t>());
     FEA_REQUIRE(!trav || p->trav_rw == rw, FEA_ERR_INVALID, "traversal record width mismatch");
-    const char* d1mode = std::getenv("FEA_D1_MODE");
-    const int ring = p->gen_on ? 0 : (d1mode ? std::atoi(d1mode) : FEA_D1_RING);
-    if (G == 4 && p->npe == 4 && trav && rw == 2 && !p->dup_nodes && sizeof(PosT) == 1 &&
-        (p->gen_on || (ring > 0 && (reinterpret_cast<uintptr_t>(K) & 15) == 0)) && !std::getenv("FEA_D1_NO_VEC")) {
-        if (ring > 0) return run_gather_d1r(p, recs, K, values, accumulate, cap, rec_stride, ring, s);
+    // npe = 4 with traversal records: direct-record kernel for a materialized K, two-lane
+    // kernel for the fused supplier
+    if (G == 4 && p->npe == 4 && trav && rw == 2 && !p->dup_nodes && sizeof(PosT) == 1 && !p->gen_on &&
+        !std::getenv("FEA_D1_NO_DIRECT")) {
+        const size_t smemg = static_cast<size_t>(kWarps) * GPW * acc_stride * sizeof(double);
+        auto kg = k_gather_d1g<FEA_D1G_U>;
+        if (smemg > 48 * 1024)
+            FEA_CK(cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemg));
+        kg<<<static_cast<unsigned>(blocks), kWarps * 32, smemg, s>>>(
+            K, p->n_own, acc_stride, accumulate ? 1 : 0, p->trav_ptr.as<int64_t>(), p->trav_meta.as<int64_t>(),
+            reinterpret_cast<const int2*>(recs.as<int32_t>()), values);
+        FEA_CK(cudaGetLastError());
+        p->last_launches += 1;
+        return;
+    }
+    if (G == 4 && p->npe == 4 && trav && rw == 2 && !p->dup_nodes && sizeof(PosT) == 1 && p->gen_on &&
+        !std::getenv("FEA_D1_NO_VEC")) {
         constexpr int GPW2 = 16;
         int acc_stride2 = std::max(p->max_cnt, 1);
         int acc_mod2 = 3;

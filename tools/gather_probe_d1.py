@@ -56,6 +56,43 @@ __global__ void probe(const double* __restrict__ K, const int* __restrict__ rec,
     const long vb = vstart[grp];
     for (int i = gl; i < vlen[grp]; i += G) __stcs(out + vb + i, s + i);
 }
+// 8-byte records {entry, slot word} and a shared-memory fold (slot = byte gl of the word mod
+// row length): the kernel's record width and accumulator traffic on the same traversal
+template <int U, bool SMEM, bool LDG>
+__global__ void probe_fold(const double* __restrict__ K, const int2* __restrict__ rec, const long* __restrict__ tptr,
+                           const long* __restrict__ vstart, const int* __restrict__ vlen, long n_nodes,
+                           double* __restrict__ out) {
+    __shared__ double acc[64 * 19];
+    const int grp = threadIdx.x >> 2, gl = threadIdx.x & 3;
+    const long node = blockIdx.x * 64L + grp;
+    long a0 = 0, a1 = 0; int rl = 1;
+    if (node < n_nodes) { a0 = tptr[node]; a1 = tptr[node + 1]; rl = vlen[node]; }
+    double* A = acc + grp * 19;
+    for (int i = gl; i < rl; i += 4) A[i] = 0;
+    double s = 0;
+    for (long c = a0; c < a1; c += U) {
+        int2 r[U]; double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) r[u] = c + u < a1 ? (LDG ? __ldg(rec + c + u) : __ldcs(rec + c + u)) : make_int2(0, 0);
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = c + u < a1 ? __ldcg(K + (long)r[u].x * 4 + gl) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (SMEM) { if (c + u < a1) { const int q = ((unsigned)r[u].y >> (8 * gl) & 0xff) % rl; A[q] += v[u]; } __syncwarp(); }
+            else s += v[u] + r[u].y;
+        }
+    }
+    __syncwarp();
+    if (node < n_nodes) { const long vb = vstart[node]; for (int i = gl; i < rl; i += 4) __stcs(out + vb + i, SMEM ? A[i] : s + i); }
+}
+void run_fold(torch::Tensor K, torch::Tensor rec2, torch::Tensor tptr, torch::Tensor vs, torch::Tensor vl, torch::Tensor out, int smem) {
+    long n = vl.numel();
+    int grid = (n + 63) / 64;
+    if (smem == 2) probe_fold<4, false, true><<<grid, 256>>>(K.data_ptr<double>(), (const int2*)rec2.data_ptr<int>(), tptr.data_ptr<long>(), vs.data_ptr<long>(), vl.data_ptr<int>(), n, out.data_ptr<double>());
+    else if (smem == 3) probe_fold<4, true, true><<<grid, 256>>>(K.data_ptr<double>(), (const int2*)rec2.data_ptr<int>(), tptr.data_ptr<long>(), vs.data_ptr<long>(), vl.data_ptr<int>(), n, out.data_ptr<double>());
+    else if (smem) probe_fold<4, true, false><<<grid, 256>>>(K.data_ptr<double>(), (const int2*)rec2.data_ptr<int>(), tptr.data_ptr<long>(), vs.data_ptr<long>(), vl.data_ptr<int>(), n, out.data_ptr<double>());
+    else probe_fold<4, false, false><<<grid, 256>>>(K.data_ptr<double>(), (const int2*)rec2.data_ptr<int>(), tptr.data_ptr<long>(), vs.data_ptr<long>(), vl.data_ptr<int>(), n, out.data_ptr<double>());
+}
 void run(torch::Tensor K, torch::Tensor rec, torch::Tensor tptr, torch::Tensor vs, torch::Tensor vl, torch::Tensor out,
          int g, int u, int bs, torch::Tensor hi, long la) {
     long n = vl.numel();
@@ -71,8 +108,8 @@ void run(torch::Tensor K, torch::Tensor rec, torch::Tensor tptr, torch::Tensor v
     if (g == 2 && u == 24) args(probe<2, 24>);
 }
 '''
-mod = load_inline("probe_d1", cpp_sources="void run(torch::Tensor K, torch::Tensor rec, torch::Tensor tptr, torch::Tensor vs, torch::Tensor vl, torch::Tensor out, int g, int u, int bs, torch::Tensor hi, long la);",
-                  cuda_sources=src, functions=["run"],
+mod = load_inline("probe_d1", cpp_sources="void run(torch::Tensor K, torch::Tensor rec, torch::Tensor tptr, torch::Tensor vs, torch::Tensor vl, torch::Tensor out, int g, int u, int bs, torch::Tensor hi, long la); void run_fold(torch::Tensor K, torch::Tensor rec2, torch::Tensor tptr, torch::Tensor vs, torch::Tensor vl, torch::Tensor out, int smem);",
+                  cuda_sources=src, functions=["run", "run_fold"],
                   extra_cuda_cflags=["-gencode", "arch=compute_100a,code=sm_100a", "-O3"], verbose=False)
 
 conn, nn, d = M.config_mesh(3)
@@ -98,10 +135,11 @@ out = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
 T = [torch.from_numpy(x).cuda() for x in (rec, tptr, vs, vl)]
 last = rec[np.maximum(tptr[1:] - 1, 0)]                          # highest K row per traversal node
 hi = torch.from_numpy(np.maximum.accumulate(last).astype(np.int32)).cuda()
+words = (rec.astype(np.uint64) * np.uint64(2654435761) >> np.uint64(7)).astype(np.uint32).view(np.int32)
+rec2 = torch.from_numpy(np.stack([rec, words], axis=1).reshape(-1).copy()).cuda()
 alg = 8 * E * 16 + 8 * plan.nnz + 4 * E * npe
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-for g, u, bs, la in [(4, 4, 128, 0), (4, 4, 256, 0), (2, 8, 128, 0), (4, 4, 128, 2048), (4, 4, 128, 8192),
-                     (4, 4, 128, 32768), (4, 4, 128, 131072), (4, 4, 256, 8192), (4, 4, 256, 32768)]:
+for g, u, bs, la in [(4, 4, 256, 0), (2, 8, 128, 0), (4, 4, 256, 8192), (4, 4, 256, 32768)]:
             mod.run(K, *T, out, g, u, bs, hi, la)
             ms = []
             for _ in range(5):
@@ -114,3 +152,17 @@ for g, u, bs, la in [(4, 4, 128, 0), (4, 4, 256, 0), (2, 8, 128, 0), (4, 4, 128,
                 ms.append(e0.elapsed_time(e1))
             t = float(np.mean(ms))
             print(f"G={g} U={u:2d} bs={bs} prefetch-ahead={la}: {t:.3f} ms  ({alg / t / 1e6:.0f} GB/s algorithmic)", flush=True)
+
+for smem in (0, 1, 2, 3):
+    mod.run_fold(K, rec2, T[1], T[2], T[3], out, smem)
+    ms = []
+    for _ in range(5):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        mod.run_fold(K, rec2, T[1], T[2], T[3], out, smem)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t = float(np.mean(ms))
+    print(f"8-byte records, U=4, {'shared-memory fold' if smem in (1, 3) else 'register sum'}, records {'ld.global.nc' if smem >= 2 else 'ld.global.cs'}: {t:.3f} ms  ({alg / t / 1e6:.0f} GB/s algorithmic)", flush=True)
