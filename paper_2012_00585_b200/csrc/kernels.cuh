@@ -948,13 +948,22 @@ __global__ void __launch_bounds__(kWarps * 32)
 #ifndef FEA_SLOT_BRANCHLESS
 #define FEA_SLOT_BRANCHLESS 1  // cfg2: 0.310 -> 0.278 ms (same bits)
 #endif
+#ifndef FEA_SLOT_WPC
+// warps per CTA. Shared memory (9.5 KB per warp on cfg2 + 1 KB reserved per CTA) caps 4-warp
+// CTAs at 5 per SM (20 warps); 8-warp CTAs fit 3 per SM (24 warps) but measured slower
+// isolated (cfg2 0.307 vs 0.277 ms: the wider node window loses L2 reuse of shared half lines)
+#define FEA_SLOT_WPC 4
+#endif
+constexpr int kSlotWarps = FEA_SLOT_WPC;
 #ifndef FEA_SLOT_MINB
-#define FEA_SLOT_MINB 6  // swept 4 (95 regs) 0.318 ms, 6 0.303, 8 0.305 on cfg2
+// register budget of 24 resident warps (swept with 4-warp CTAs: 4 (95 regs) 0.318 ms,
+// 6 0.303, 8 0.305 on cfg2)
+#define FEA_SLOT_MINB (24 / FEA_SLOT_WPC)
 #endif
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 template <int D, int NPE, bool DISTINCT, bool GEN>
-__global__ void __launch_bounds__(kWarps * 32, FEA_SLOT_MINB)
+__global__ void __launch_bounds__(kSlotWarps * 32, FEA_SLOT_MINB)
     k_gather_slot(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
                   const int32_t* __restrict__ adj, const uint8_t* __restrict__ posA,
                   const int64_t* __restrict__ nptr, const int32_t* __restrict__ order, int64_t n_own,
@@ -968,8 +977,8 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_SLOT_MINB)
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     double* wbuf = sbuf + static_cast<int64_t>(warp) * 2 * nbuf * dm;
-    const int64_t W = static_cast<int64_t>(gridDim.x) * kWarps;
-    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+    const int64_t W = static_cast<int64_t>(gridDim.x) * kSlotWarps;
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kSlotWarps + warp;
 
     // per-node pipeline: incidence range 3 nodes ahead, records (entry, position words) and
     // row info 2 ahead, chunk copies 1 ahead, fold of the current node
@@ -1039,12 +1048,12 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_SLOT_MINB)
         return R;
     };
     // per-warp inverse position table: inv[k*32 + slot] = element column + 1 (0: none)
-    uint8_t* inv = reinterpret_cast<uint8_t*>(sbuf + static_cast<int64_t>(kWarps) * 2 * nbuf * dm) +
+    uint8_t* inv = reinterpret_cast<uint8_t*>(sbuf + static_cast<int64_t>(kSlotWarps) * 2 * nbuf * dm) +
                    static_cast<int64_t>(warp) * nbuf * 32;
 #if FEA_SLOT_TMA
     // one mbarrier per buffer; lane k issues block k as ONE bulk copy (TMA), completion by bytes
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sbuf) +
-                                                 static_cast<int64_t>(kWarps) * nbuf * (2 * dm * 8 + 32)) +
+                                                 static_cast<int64_t>(kSlotWarps) * nbuf * (2 * dm * 8 + 32)) +
                      2 * warp;
     if (!GEN && lane == 0) {
         mbar_init(smem_u32(bars), 1);
@@ -1657,7 +1666,7 @@ void run_gather_slot(fea_plan* p, const Incidences& in, const double* K, double*
                      cudaStream_t s) {
     const int dm = D * D * NPE;
     const int nbuf = static_cast<int>(std::max<int64_t>(p->max_adj, 1));
-    const size_t smem = static_cast<size_t>(kWarps) * nbuf * (2 * dm * sizeof(double) + 32) + kWarps * 16;
+    const size_t smem = static_cast<size_t>(kSlotWarps) * nbuf * (2 * dm * sizeof(double) + 32) + kSlotWarps * 16;
     auto kern = p->gen_on ? (p->dup_nodes ? k_gather_slot<D, NPE, false, true> : k_gather_slot<D, NPE, true, true>)
                           : (p->dup_nodes ? k_gather_slot<D, NPE, false, false> : k_gather_slot<D, NPE, true, false>);
     if (smem > 48 * 1024)
@@ -1665,11 +1674,11 @@ void run_gather_slot(fea_plan* p, const Incidences& in, const double* K, double*
     int dev = 0, sms = 148, per_sm = 1;
     FEA_CK(cudaGetDevice(&dev));
     FEA_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    FEA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem));
-    const int64_t want = (p->n_own + kWarps - 1) / kWarps;  // one node per warp at most
+    FEA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSlotWarps * 32, smem));
+    const int64_t want = (p->n_own + kSlotWarps - 1) / kSlotWarps;  // one node per warp at most
     const int64_t blocks = std::min<int64_t>(want, static_cast<int64_t>(sms) * std::max(per_sm, 1));
     if (blocks == 0) return;
-    kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
+    kern<<<static_cast<unsigned>(blocks), kSlotWarps * 32, smem, s>>>(
         K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const uint8_t*>(in.posA), p->nptr.as<int64_t>(),
         p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, nbuf, accumulate ? 1 : 0,
         gen_of(p), values);
@@ -1678,14 +1687,14 @@ void run_gather_slot(fea_plan* p, const Incidences& in, const double* K, double*
 }
 
 // lane = slot kernel applies: d in {2,3,4}, element rows of <= 8 nodes with byte positions,
-// node rows of <= 32 column nodes, <= 32 incidences per node, 16-byte chunks, <= 96 KB smem
+// node rows of <= 32 column nodes, <= 32 incidences per node, 16-byte chunks, <= 24 KB smem per warp
 bool slot_applies(const fea_plan* p) {
     if (p->d < 2 || p->d > 4 || (p->npe != 4 && p->npe != 8) || p->pos_bytes != 1 || p->max_cnt > 32 ||
         p->max_adj > 32 || p->gen_on)
         return false;
     const int64_t dm = static_cast<int64_t>(p->d) * p->d * p->npe;
     if (dm % 2) return false;
-    return static_cast<int64_t>(kWarps) * 2 * std::max<int64_t>(p->max_adj, 1) * dm * 8 <= 96 * 1024;
+    return 2 * std::max<int64_t>(p->max_adj, 1) * dm * 8 <= 24 * 1024;  // per-warp double buffer
 }
 
 #ifndef FEA_CN_PF8
