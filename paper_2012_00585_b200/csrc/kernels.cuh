@@ -655,6 +655,124 @@ __global__ void __launch_bounds__(kWarps * 32, cn_min_blocks<G, PF>())
     for (int i = gl; i < block; i += G) __stcs(values + vb + i, acc[i]);
 }
 
+// Fixed-stride record form of k_gather_cn for warp-wide groups (G = 32: hex27, npe <= 28,
+// <= 8 incidences per node, byte positions). k_gather_cn's node prologue is
+// a chain of three memory round trips — adj_ptr / nptr, then the incidence entries and position
+// rows at adj_ptr[v], then the K row blocks — and with ~3.3 incidences per hex27 node it is a
+// third of the kernel's stall samples. Here a plan-time table holds, per traversal node at a
+// fixed stride, a 16-byte header (values start, row length, incidence count, packed
+// accumulator offset) and the node's incidence records {entry, position bytes} (8 x 32 B; one
+// table per incidence order, so FEA_DET_COLOUR reads its colour-ordered records the same way):
+// the warp loads both with one round trip (no adj_ptr dependence), then the K row blocks.
+// Fold as k_gather_cn: ascending element id per slot, bit-identical.
+constexpr int kCnrSlots = 8;   // incidence records per node
+constexpr int kCnrBytes = 32;  // bytes per record: int32 entry + up to 28 position bytes
+__global__ void k_cnr_build(const int32_t* __restrict__ order, const int64_t* __restrict__ adj_ptr,
+                            const int32_t* __restrict__ adj, const uint8_t* __restrict__ posA,
+                            const int64_t* __restrict__ nptr, int64_t n_own, int npe, int pstride, int d,
+                            int per_cta, int4* __restrict__ hdr, int32_t* __restrict__ rec) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_own;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = order != nullptr ? order[t] : t;
+        const int64_t b0 = adj_ptr[v];
+        const int n = static_cast<int>(adj_ptr[v + 1] - b0);
+        const int64_t c0 = nptr[v];
+        const int cnt = static_cast<int>(nptr[v + 1] - c0);
+        int64_t acc_off = 0;  // packed accumulators: blocks (+1 stagger) of the CTA's earlier groups
+        for (int64_t g = t - t % per_cta; g < t; ++g) {
+            const int64_t u = order != nullptr ? order[g] : g;
+            acc_off += static_cast<int64_t>(d) * d * (nptr[u + 1] - nptr[u]) + 1;
+        }
+        const int64_t vb = static_cast<int64_t>(d) * d * c0;
+        hdr[t] = make_int4(static_cast<int>(vb & 0xffffffff), static_cast<int>(vb >> 32),
+                           d * cnt | (n << 16), static_cast<int>(acc_off));
+        int32_t* r = rec + t * (kCnrSlots * kCnrBytes / 4);
+        for (int k = 0; k < kCnrSlots; ++k) {
+            uint32_t w[kCnrBytes / 4];
+            for (int q = 0; q < kCnrBytes / 4; ++q) w[q] = 0;
+            if (k < n) {
+                w[0] = static_cast<uint32_t>(adj[b0 + k]);
+                for (int b = 0; b < npe; ++b)
+                    w[1 + b / 4] |= static_cast<uint32_t>(posA[(b0 + k) * pstride + b]) << (8 * (b & 3));
+            }
+            for (int q = 0; q < kCnrBytes / 4; ++q) r[k * (kCnrBytes / 4) + q] = static_cast<int32_t>(w[q]);
+        }
+    }
+}
+
+#ifndef FEA_CNR_MINB
+#define FEA_CNR_MINB 6
+#endif
+#ifndef FEA_CNR_PF
+#define FEA_CNR_PF 2
+#endif
+template <int D, int PF>
+__global__ void __launch_bounds__(kWarps * 32, FEA_CNR_MINB)
+    k_gather_cnr(const double* __restrict__ K, const int4* __restrict__ hdr, const int2* __restrict__ rec,
+                 int64_t n_own, int npe, int accumulate, int64_t cta_acc, double* __restrict__ values) {
+    extern __shared__ double sacc[];
+    constexpr int R = D * D;
+    const int m = D * npe;
+    const int dm = D * m;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const bool col_ok = lane < npe;
+    const int64_t vi = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+    // one round trip: header and the node's 8 records (lane l: 8 bytes of the 256-byte block)
+    int4 h = make_int4(0, 0, 0, 0);
+    int2 rw = make_int2(0, 0);
+    if (vi < n_own) {
+        h = __ldg(hdr + vi);
+        rw = __ldcs(rec + vi * 32 + lane);
+    }
+    int2* srec = reinterpret_cast<int2*>(sacc + cta_acc) + warp * 32;
+    srec[lane] = rw;
+    const int64_t vb = static_cast<int64_t>(static_cast<uint32_t>(h.x)) | (static_cast<int64_t>(h.y) << 32);
+    const int rowlen = h.z & 0xffff;
+    const int n = h.z >> 16;
+    const int block = D * rowlen;
+    double* acc = sacc + h.w;
+    const uint8_t* spos = reinterpret_cast<const uint8_t*>(srec);
+    const int32_t* sent = reinterpret_cast<const int32_t*>(srec);
+    __syncwarp();
+    double kv[PF][R];
+    auto load = [&](int p, int k) {
+        if (k < n && col_ok) {
+            const double* src = K + static_cast<int64_t>(sent[k * (kCnrBytes / 4)]) * dm + lane * D;
+#pragma unroll
+            for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+                for (int kj = 0; kj < D; ++kj) kv[p][ki * D + kj] = __ldg(src + ki * m + kj);
+        }
+    };
+#pragma unroll
+    for (int p = 0; p < PF; ++p) load(p, p);
+    for (int i = lane; i < block; i += 32) acc[i] = accumulate ? values[vb + i] : 0.0;
+    __syncwarp();
+    for (int k0 = 0; k0 < n; k0 += PF) {  // n is warp-uniform (one node per warp)
+#pragma unroll
+        for (int p = 0; p < PF; ++p) {
+            const int k = k0 + p;
+            if (k < n && col_ok) {
+                const int base = static_cast<int>(spos[k * kCnrBytes + 4 + lane]) * D;
+                FEA_DCHECK(base + (D - 1) * rowlen + D - 1 < block);
+                double a[R];
+#pragma unroll
+                for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+                    for (int kj = 0; kj < D; ++kj) a[ki * D + kj] = acc[ki * rowlen + base + kj];
+#pragma unroll
+                for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+                    for (int kj = 0; kj < D; ++kj) acc[ki * rowlen + base + kj] = a[ki * D + kj] + kv[p][ki * D + kj];
+            }
+            __syncwarp();
+            load(p, k + PF);
+        }
+    }
+    for (int i = lane; i < block; i += 32) __stcs(values + vb + i, acc[i]);
+}
+
 // ---------------------------------------------------------------------------
 // Deterministic owner-computes gather for one DOF per node (d = 1): staged incidences
 // ---------------------------------------------------------------------------
@@ -1748,6 +1866,35 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
     const size_t smem = static_cast<size_t>(cta_acc) * sizeof(double) +
                         static_cast<size_t>(kWarps) * GPW * pos_stride * sizeof(PosT);
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
+    if (G == 32 && sizeof(PosT) == 1 && !p->gen_on && !p->dup_nodes && p->max_adj <= kCnrSlots &&
+        p->npe <= kCnrBytes - 4 && (in.adj == p->adj.as<int32_t>() || in.adj == p->adjC.as<int32_t>()) &&
+        !std::getenv("FEA_CN_NO_RECORDS")) {
+        // built lazily on the first assembly of each incidence order: 16 + 256 bytes per node
+        feagpu::DevBuf& recs = in.adj == p->adj.as<int32_t>() ? p->cnr_rec : p->cnr_recC;
+        if (!p->cnr_hdr.p || !recs.p) {
+            if (!p->cnr_hdr.p) p->cnr_hdr.alloc(std::max<int64_t>(p->n_own, 1) * 16);
+            recs.alloc(std::max<int64_t>(p->n_own, 1) * kCnrSlots * kCnrBytes);
+            if (p->n_own > 0) {
+                k_cnr_build<<<grid_for(p->n_own, 256), 256, 0, s>>>(
+                    p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->adj_ptr.as<int64_t>(), in.adj,
+                    static_cast<const uint8_t*>(in.posA), p->nptr.as<int64_t>(), p->n_own, p->npe, p->pstride,
+                    p->d, kWarps, p->cnr_hdr.as<int4>(), recs.as<int32_t>());
+                FEA_CK(cudaGetLastError());
+            }
+        }
+        const size_t smem_r = static_cast<size_t>(cta_acc) * sizeof(double) + kWarps * kCnrSlots * kCnrBytes;
+        FEA_REQUIRE(smem_r <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
+        auto kr = k_gather_cnr<D, FEA_CNR_PF>;
+        if (smem_r > 48 * 1024)
+            FEA_CK(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
+        const int64_t blocks_r = (p->n_own + kWarps - 1) / kWarps;
+        if (blocks_r == 0) return;
+        kr<<<static_cast<unsigned>(blocks_r), kWarps * 32, smem_r, s>>>(
+            K, p->cnr_hdr.as<int4>(), recs.as<int2>(), p->n_own, p->npe, accumulate ? 1 : 0, cta_acc, values);
+        FEA_CK(cudaGetLastError());
+        p->last_launches += 1;
+        return;
+    }
     auto kern = p->gen_on ? (p->dup_nodes ? k_gather_cn<G, D, PF, PosT, false, true>
                                           : k_gather_cn<G, D, PF, PosT, true, true>)
                           : (p->dup_nodes ? k_gather_cn<G, D, PF, PosT, false, false>
