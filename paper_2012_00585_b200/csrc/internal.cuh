@@ -113,6 +113,7 @@ struct fea_plan {
     feagpu::DevBuf cnr_hdr;    // int4 [n_own]: values start (int64), row length | n << 16, accumulator offset
     feagpu::DevBuf cnr_rec;    // [n_own][8][32 B]: {entry, npe position bytes} per incidence (k_gather_cnr)
     feagpu::DevBuf cnr_recC;   // the same for the colour-ordered incidences (reset by set_colouring)
+    feagpu::DevBuf slot_hdr, slot_rec, slot_recC;  // k_gather_slot fixed-stride node metadata (lazy)
     int32_t trav_rw = 0;
     int64_t cn_cta_acc = 0;     // packed accumulator doubles per CTA of k_gather_cn (lazy)
     int32_t cn_cta_per = 0;

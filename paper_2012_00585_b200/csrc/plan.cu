@@ -1065,6 +1065,7 @@ void build_colour_incidences(fea_plan* p, const std::vector<int32_t>& colour_of_
     // sequentially like the sorted route
     p->trav_recC.reset();
     p->cnr_recC.reset();
+    p->slot_recC.reset();
     if (p->trav_rec.p) {
         const int pw = p->pstride * p->pos_bytes / 4;
         p->trav_recC.alloc(std::max<int64_t>(n, 1) * p->trav_rw * 4);
@@ -1086,7 +1087,7 @@ int64_t metadata_bytes(const fea_plan* p) {
                                 p->order.bytes + p->at_krow.bytes + p->at_rows.bytes + p->at_pos.bytes + p->colour_elems.bytes + p->adjC.bytes + p->posAC.bytes +
                                 p->node_order.bytes + p->trav_ptr.bytes + p->trav_meta.bytes +
                                 p->trav_rec.bytes + p->trav_recC.bytes + p->cnr_hdr.bytes + p->cnr_rec.bytes +
-                                p->cnr_recC.bytes);
+                                p->cnr_recC.bytes + p->slot_hdr.bytes + p->slot_rec.bytes + p->slot_recC.bytes);
 }
 
 }  // namespace feagpu
