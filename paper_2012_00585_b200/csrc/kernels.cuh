@@ -706,10 +706,10 @@ __global__ void k_cnr_build(const int32_t* __restrict__ order, const int64_t* __
 #ifndef FEA_CNR_PF
 #define FEA_CNR_PF 2
 #endif
-template <int D, int PF>
+template <int D, int PF, bool GEN>
 __global__ void __launch_bounds__(kWarps * 32, FEA_CNR_MINB)
     k_gather_cnr(const double* __restrict__ K, const int4* __restrict__ hdr, const int2* __restrict__ rec,
-                 int64_t n_own, int npe, int accumulate, int64_t cta_acc, double* __restrict__ values) {
+                 int64_t n_own, int npe, int accumulate, int64_t cta_acc, GenK gen, double* __restrict__ values) {
     extern __shared__ double sacc[];
     constexpr int R = D * D;
     const int m = D * npe;
@@ -738,11 +738,22 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_CNR_MINB)
     double kv[PF][R];
     auto load = [&](int p, int k) {
         if (k < n && col_ok) {
-            const double* src = K + static_cast<int64_t>(sent[k * (kCnrBytes / 4)]) * dm + lane * D;
+            const int32_t entry = sent[k * (kCnrBytes / 4)];
+            if (GEN) {  // fused supplier: generate the d x d sub-block in registers
+                const int64_t krow = entry / npe;
+                const int a = static_cast<int>(entry - krow * npe);
+                const uint64_t he = kgen_elem(gen.seed, gen.ids ? gen.ids[krow] : krow);
 #pragma unroll
-            for (int ki = 0; ki < D; ++ki)
+                for (int ki = 0; ki < D; ++ki)
 #pragma unroll
-                for (int kj = 0; kj < D; ++kj) kv[p][ki * D + kj] = __ldg(src + ki * m + kj);
+                    for (int kj = 0; kj < D; ++kj) kv[p][ki * D + kj] = kgen_entry(he, a * D + ki, lane * D + kj);
+            } else {
+                const double* src = K + static_cast<int64_t>(entry) * dm + lane * D;
+#pragma unroll
+                for (int ki = 0; ki < D; ++ki)
+#pragma unroll
+                    for (int kj = 0; kj < D; ++kj) kv[p][ki * D + kj] = __ldg(src + ki * m + kj);
+            }
         }
     };
 #pragma unroll
@@ -1927,7 +1938,7 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
     const size_t smem = static_cast<size_t>(cta_acc) * sizeof(double) +
                         static_cast<size_t>(kWarps) * GPW * pos_stride * sizeof(PosT);
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
-    if (G == 32 && sizeof(PosT) == 1 && !p->gen_on && !p->dup_nodes && p->max_adj <= kCnrSlots &&
+    if (G == 32 && sizeof(PosT) == 1 && !p->dup_nodes && p->max_adj <= kCnrSlots &&
         p->npe <= kCnrBytes - 4 && (in.adj == p->adj.as<int32_t>() || in.adj == p->adjC.as<int32_t>()) &&
         !std::getenv("FEA_CN_NO_RECORDS")) {
         // built lazily on the first assembly of each incidence order: 16 + 256 bytes per node
@@ -1945,13 +1956,14 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
         }
         const size_t smem_r = static_cast<size_t>(cta_acc) * sizeof(double) + kWarps * kCnrSlots * kCnrBytes;
         FEA_REQUIRE(smem_r <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
-        auto kr = k_gather_cnr<D, FEA_CNR_PF>;
+        auto kr = p->gen_on ? k_gather_cnr<D, FEA_CNR_PF, true> : k_gather_cnr<D, FEA_CNR_PF, false>;
         if (smem_r > 48 * 1024)
             FEA_CK(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
         const int64_t blocks_r = (p->n_own + kWarps - 1) / kWarps;
         if (blocks_r == 0) return;
         kr<<<static_cast<unsigned>(blocks_r), kWarps * 32, smem_r, s>>>(
-            K, p->cnr_hdr.as<int4>(), recs.as<int2>(), p->n_own, p->npe, accumulate ? 1 : 0, cta_acc, values);
+            K, p->cnr_hdr.as<int4>(), recs.as<int2>(), p->n_own, p->npe, accumulate ? 1 : 0, cta_acc, gen_of(p),
+            values);
         FEA_CK(cudaGetLastError());
         p->last_launches += 1;
         return;
