@@ -516,3 +516,32 @@ def test_random_unstructured_meshes(gpu, orc, seed):
         plan.set_colouring(col)
         assert plan.assemble(K, strategy="colour").cpu().numpy().tobytes() == want_col.tobytes()
         assert close(plan.assemble(K, strategy="atomic").cpu().numpy(), want)
+
+
+KERNEL_SWITCHES = ["FEA_SLOT_NO_FIXED", "FEA_CN_NO_RECORDS", "FEA_D1_NO_DIRECT", "FEA_D1_NO_VEC",
+                   "FEA_GATHER_NO_SLOT", "FEA_GATHER_NO_CN"]
+
+
+@pytest.mark.parametrize("switch", KERNEL_SWITCHES)
+@pytest.mark.parametrize("mesh,n,d,perm", [("hex8", 3, 3, "elements"), ("tet4", 4, 1, "nodes"),
+                                            ("hex27", 2, 3, None)])
+def test_kernel_switches_same_bits(gpu, orc, switch, mesh, n, d, perm, monkeypatch):
+    """Every A/B switch selects another kernel of the same route: the sorted and
+    colour routes and the fused supplier stay bit-identical to the oracle / the default path."""
+    import torch
+    conn, nn, ed, n_rows = problem(mesh, n, d, perm)
+    E, m = ed.shape
+    P = orc.Pattern.build(conn, nn, d)
+    Kh = orc.fill_k(42, E, m)
+    want = P.assemble_sequential(ed, Kh)
+    col, _ = orc.greedy_colouring(conn, nn)
+    want_col = P.assemble_coloured(ed, Kh, col)
+    K = torch.from_numpy(Kh).cuda()
+    monkeypatch.setenv(switch, "1")
+    with gpu.Plan(ed, n_rows, dofs_per_node=d) as plan:
+        assert plan.assemble(K, strategy="sorted").cpu().numpy().tobytes() == want.tobytes()
+        plan.set_colouring(col)
+        assert plan.assemble(K, strategy="colour").cpu().numpy().tobytes() == want_col.tobytes()
+        Ks = gpu.fill_seeded_k(E, m, 11)
+        ref = plan.assemble(Ks, strategy="sorted").cpu().numpy()
+        assert plan.assemble_seeded(11, strategy="sorted").cpu().numpy().tobytes() == ref.tobytes()
