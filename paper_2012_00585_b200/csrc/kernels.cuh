@@ -18,6 +18,13 @@ constexpr int kWarps = 4;  // warps per CTA for the numeric kernels
 
 
 
+// lazily built plan tables are allocated on first use; inside a stream capture (CUDA graph)
+// allocation is not allowed, so the kernels that read them fall back to the table-free path
+bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone;
+}
+
 unsigned grid_for(int64_t n, int threads) {
     int64_t b = (n + threads - 1) / threads;
     if (b < 1) b = 1;
@@ -1845,8 +1852,9 @@ void run_gather_slot(fea_plan* p, const Incidences& in, const double* K, double*
     const size_t smem = static_cast<size_t>(kSlotWarps) * nbuf * (2 * dm * sizeof(double) + 32) + kSlotWarps * 16;
     // fixed-stride metadata table per incidence order (lazily; 16 + 16 * nbuf bytes per node)
     const bool sorted_inc = in.adj == p->adj.as<int32_t>();
-    const bool fixed = !p->gen_on && (sorted_inc || in.adj == p->adjC.as<int32_t>()) && !std::getenv("FEA_SLOT_NO_FIXED");
     feagpu::DevBuf& fx = sorted_inc ? p->slot_rec : p->slot_recC;
+    const bool fixed = !p->gen_on && (sorted_inc || in.adj == p->adjC.as<int32_t>()) &&
+                       !std::getenv("FEA_SLOT_NO_FIXED") && (fx.p || !capturing(s));
     if (fixed && !fx.p) {
         if (!p->slot_hdr.p) p->slot_hdr.alloc(std::max<int64_t>(p->n_own, 1) * 16);
         fx.alloc(std::max<int64_t>(p->n_own, 1) * nbuf * 16);
@@ -1940,7 +1948,8 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
     if (G == 32 && sizeof(PosT) == 1 && !p->dup_nodes && p->max_adj <= kCnrSlots &&
         p->npe <= kCnrBytes - 4 && (in.adj == p->adj.as<int32_t>() || in.adj == p->adjC.as<int32_t>()) &&
-        !std::getenv("FEA_CN_NO_RECORDS")) {
+        !std::getenv("FEA_CN_NO_RECORDS") &&
+        ((p->cnr_hdr.p && (in.adj == p->adj.as<int32_t>() ? p->cnr_rec.p : p->cnr_recC.p)) || !capturing(s))) {
         // built lazily on the first assembly of each incidence order: 16 + 256 bytes per node
         feagpu::DevBuf& recs = in.adj == p->adj.as<int32_t>() ? p->cnr_rec : p->cnr_recC;
         if (!p->cnr_hdr.p || !recs.p) {

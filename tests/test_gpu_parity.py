@@ -545,3 +545,38 @@ def test_kernel_switches_same_bits(gpu, orc, switch, mesh, n, d, perm, monkeypat
         Ks = gpu.fill_seeded_k(E, m, 11)
         ref = plan.assemble(Ks, strategy="sorted").cpu().numpy()
         assert plan.assemble_seeded(11, strategy="sorted").cpu().numpy().tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("mesh,n,d,perm", [("hex8", 3, 3, "elements"), ("tet4", 4, 1, "nodes"),
+                                            ("hex27", 2, 3, None)])
+def test_cuda_graph_replay(gpu, orc, mesh, n, d, perm):
+    """After one warm-up call per route (which builds the lazily created plan tables), the
+    assembly is stream-ordered with no host synchronisation: it can be captured in a CUDA graph
+    and replayed (the launch-bound inner loop of a Newton / time-stepping caller)."""
+    import torch
+    conn, nn, ed, n_rows = problem(mesh, n, d, perm)
+    E, m = ed.shape
+    P = orc.Pattern.build(conn, nn, d)
+    Kh = orc.fill_k(42, E, m)
+    want = P.assemble_sequential(ed, Kh)
+    K = torch.from_numpy(Kh).cuda()
+    with gpu.Plan(ed, n_rows, dofs_per_node=d) as plan:
+        plan.set_colouring(plan.greedy_colouring()[0])
+        for strategy in ("sorted", "colour", "atomic"):
+            v = torch.zeros(plan.nnz, dtype=torch.float64, device="cuda")
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                plan.assemble(K, v, strategy=strategy, stream=s)  # warm-up: lazy tables
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                v.zero_()
+                plan.assemble(K, v, strategy=strategy, accumulate=True, stream=s)
+            v.fill_(7.0)
+            g.replay()
+            torch.cuda.synchronize()
+            got = v.cpu().numpy()
+            if strategy == "atomic":
+                assert close(got, want)
+            elif strategy == "sorted":
+                assert got.tobytes() == want.tobytes()
