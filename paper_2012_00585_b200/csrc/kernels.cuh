@@ -1133,7 +1133,7 @@ __global__ void __launch_bounds__(kSlotWarps * 32, FEA_SLOT_MINB)
     k_gather_slot(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr,
                   const int32_t* __restrict__ adj, const uint8_t* __restrict__ posA,
                   const int64_t* __restrict__ nptr, const int32_t* __restrict__ order, int64_t n_own,
-                  int nbuf, int accumulate, GenK gen, const int4* __restrict__ shdr,
+                  int nbuf, int istr, int accumulate, GenK gen, const int4* __restrict__ shdr,
                   const int4* __restrict__ srec, double* __restrict__ values) {
     extern __shared__ double sbuf[];
     constexpr int PW = NPE <= 4 ? 1 : 2;  // position words per incidence
@@ -1229,13 +1229,14 @@ __global__ void __launch_bounds__(kSlotWarps * 32, FEA_SLOT_MINB)
         }
         return R;
     };
-    // per-warp inverse position table: inv[k*32 + slot] = element column + 1 (0: none)
+    // per-warp inverse position table: inv[k*istr + slot] = element column + 1 (0: none);
+    // istr = the longest node row rounded to 4 bytes (<= 32)
     uint8_t* inv = reinterpret_cast<uint8_t*>(sbuf + static_cast<int64_t>(kSlotWarps) * 2 * nbuf * dm) +
-                   static_cast<int64_t>(warp) * nbuf * 32;
+                   static_cast<int64_t>(warp) * nbuf * istr;
 #if FEA_SLOT_TMA
     // one mbarrier per buffer; lane k issues block k as ONE bulk copy (TMA), completion by bytes
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sbuf) +
-                                                 static_cast<int64_t>(kSlotWarps) * nbuf * (2 * dm * 8 + 32)) +
+                                                 static_cast<int64_t>(kSlotWarps) * nbuf * (2 * dm * 8 + istr)) +
                      2 * warp;
     if (!GEN && lane == 0) {
         mbar_init(smem_u32(bars), 1);
@@ -1312,7 +1313,7 @@ __global__ void __launch_bounds__(kSlotWarps * 32, FEA_SLOT_MINB)
         if constexpr (DISTINCT && !GEN) {
             // slots of one element are distinct: invert the position bytes once per node
             uint32_t* inv32 = reinterpret_cast<uint32_t*>(inv);
-            for (int i = lane; i < Rc.n * 8; i += 32) inv32[i] = 0u;
+            for (int i = lane; i < Rc.n * (istr / 4); i += 32) inv32[i] = 0u;
             __syncwarp();
             for (int base = 0; base < Rc.n * NPE; base += 32) {  // warp-uniform trip count (shuffles)
                 const int q = base + lane;
@@ -1321,12 +1322,12 @@ __global__ void __launch_bounds__(kSlotWarps * 32, FEA_SLOT_MINB)
                 const uint32_t w0 = __shfl_sync(0xffffffffu, Rc.pw[0], k & 31);
                 const uint32_t w1 = PW == 1 ? w0 : __shfl_sync(0xffffffffu, Rc.pw[PW - 1], k & 31);
                 const uint32_t w = col < 4 ? w0 : w1;
-                if (q < Rc.n * NPE) inv[k * 32 + ((w >> (8 * (col & 3))) & 0xffu)] = static_cast<uint8_t>(col + 1);
+                if (q < Rc.n * NPE) inv[k * istr + ((w >> (8 * (col & 3))) & 0xffu)] = static_cast<uint8_t>(col + 1);
             }
             __syncwarp();
             if (mine) {
                 for (int k = 0; k < Rc.n; ++k) {
-                    const int c = inv[k * 32 + lane];
+                    const int c = inv[k * istr + lane];
                     if (c) {
                         const double* src = cb + k * dm + (c - 1) * D;
 #pragma unroll
@@ -1849,7 +1850,16 @@ void run_gather_slot(fea_plan* p, const Incidences& in, const double* K, double*
                      cudaStream_t s) {
     const int dm = D * D * NPE;
     const int nbuf = static_cast<int>(std::max<int64_t>(p->max_adj, 1));
-    const size_t smem = static_cast<size_t>(kSlotWarps) * nbuf * (2 * dm * sizeof(double) + 32) + kSlotWarps * 16;
+#ifndef FEA_SLOT_TIGHT_INV
+#define FEA_SLOT_TIGHT_INV 0
+#endif
+    // inverse-table row: 32 bytes, or (FEA_SLOT_TIGHT_INV) the longest node row rounded to 4
+    // bytes: on hex8 (27 column nodes) 28 bytes per block bring a 4-warp CTA to 37,824 B and 6
+    // CTAs per SM instead of 5 — faster only when the clock is power-capped (bench 0.292 vs
+    // 0.305 ms at ~1,610-1,680 MHz), slower at full clock (0.312 vs 0.280 ms at 1,965 MHz;
+    // cfg5 20.9 vs 17.6 ms), like 8-warp CTAs: not the default
+    const int istr = FEA_SLOT_TIGHT_INV ? std::max(4, (p->max_cnt + 3) & ~3) : 32;
+    const size_t smem = static_cast<size_t>(kSlotWarps) * nbuf * (2 * dm * sizeof(double) + istr) + kSlotWarps * 16;
     // fixed-stride metadata table per incidence order (lazily; 16 + 16 * nbuf bytes per node)
     const bool sorted_inc = in.adj == p->adj.as<int32_t>();
     feagpu::DevBuf& fx = sorted_inc ? p->slot_rec : p->slot_recC;
@@ -1878,7 +1888,7 @@ void run_gather_slot(fea_plan* p, const Incidences& in, const double* K, double*
     if (blocks == 0) return;
     kern<<<static_cast<unsigned>(blocks), kSlotWarps * 32, smem, s>>>(
         K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const uint8_t*>(in.posA), p->nptr.as<int64_t>(),
-        p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, nbuf, accumulate ? 1 : 0,
+        p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, nbuf, istr, accumulate ? 1 : 0,
         gen_of(p), fixed ? p->slot_hdr.as<int4>() : nullptr, fixed ? fx.as<int4>() : nullptr, values);
     FEA_CK(cudaGetLastError());
     p->last_launches += 1;
