@@ -185,6 +185,14 @@ FEA_API fea_status fea_assemble(fea_plan* plan, const double* K, int32_t strateg
 FEA_API fea_status fea_assemble_host(fea_plan* plan, const double* K_host, int32_t strategy,
                              double* values_host, uint32_t flags, void* stream);
 
+/* Pipeline depth of fea_assemble_host: the node traversal is cut into n_windows windows; K
+ * goes host->device in the chunks each window first needs, every window is launched as soon as
+ * its chunk has landed and its values range goes device->host while later chunks are still
+ * coming in (contiguous ranges when nodes are traversed in id order). 0 (default): automatic,
+ * chunks of >= 256 MB of K and at most 32 windows. Only the segmented-reduction routes whose
+ * kernels take windows use them; the others run upload -> assemble -> download. */
+FEA_API fea_status fea_plan_set_host_windows(fea_plan* plan, int32_t n_windows);
+
 /* Fused supplier: assemble the seeded synthetic element matrices of fea_fill_seeded_k WITHOUT
  * materializing K — the gather kernels generate each entry in registers (the GPU form of the
  * reference's ElementMatrixSupplier called inside the assembly, assembly.hpp:37, :78). Same bits

@@ -49,6 +49,7 @@ def orc():
         L.orc_splitmix64.restype = c_uint64
         L.orc_splitmix64.argtypes = [c_uint64]
         L.orc_fill_k.argtypes = [c_uint64, c_int64, c_int32, c_void_p]
+        L.orc_fill_k_range.argtypes = [c_uint64, c_int64, c_int64, c_int32, c_void_p]
         L.orc_build_pattern.restype = c_void_p
         L.orc_build_pattern.argtypes = [c_void_p, c_int64, c_int, c_int64, c_int]
         L.orc_pattern_from_arrays.restype = c_void_p
@@ -164,9 +165,22 @@ def greedy_colouring(conn, n_nodes: int):
     return col, n
 
 
-def fill_k(seed: int, n: int, m: int) -> np.ndarray:
+def fill_k(seed: int, n: int, m: int, e0: int = 0, threads: int = 0) -> np.ndarray:
+    """Seeded K of elements e0 .. e0+n-1 (orc_kval), filled by `threads` host threads
+    (0: all cores; ctypes releases the GIL)."""
     K = np.empty((n, m, m), np.float64)
-    orc().orc_fill_k(seed, n, m, _p(K))
+    if n == 0:
+        return K
+    threads = threads or (os.cpu_count() or 1)
+    step = max(4096, (n + threads - 1) // threads)
+    L = orc()
+    if threads == 1 or n <= step:
+        L.orc_fill_k_range(seed, e0, n, m, _p(K))
+        return K
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda a: L.orc_fill_k_range(seed, e0 + a, min(step, n - a), m, c_void_p(K[a:].ctypes.data)),
+                    range(0, n, step)))
     return K
 
 

@@ -48,6 +48,14 @@ void orc_fill_k(uint64_t seed, int64_t n_elements, int32_t m, double* K) {
             for (int32_t j = 0; j < m; ++j) K[(e * m + i) * m + j] = orc_kval(seed, e, i, j);
 }
 
+/* K of elements e0 .. e0+n-1 (element ids, not positions) into K[0 .. n*m*m): lets the
+ * Python side fill large buffers from several threads. */
+void orc_fill_k_range(uint64_t seed, int64_t e0, int64_t n, int32_t m, double* K) {
+    for (int64_t e = 0; e < n; ++e)
+        for (int32_t i = 0; i < m; ++i)
+            for (int32_t j = 0; j < m; ++j) K[(e * m + i) * m + j] = orc_kval(seed, e0 + e, i, j);
+}
+
 /* ------------------------------------------------------------------------ */
 /* Symbolic phase                                                            */
 /* ------------------------------------------------------------------------ */

@@ -53,6 +53,7 @@ SIGNATURES = {
     "fea_plan_jp_colouring": (c_int, [c_void_p, c_uint64, c_void_p, _P32]),
     "fea_assemble": (c_int, [c_void_p, c_void_p, c_int32, c_void_p, c_uint32, c_void_p]),
     "fea_assemble_host": (c_int, [c_void_p, c_void_p, c_int32, c_void_p, c_uint32, c_void_p]),
+    "fea_plan_set_host_windows": (c_int, [c_void_p, c_int32]),
     "fea_assemble_host_batch": (c_int, [c_void_p, POINTER(c_void_p), c_int32, POINTER(c_void_p),
                                         c_int32, c_uint32, c_void_p]),
     "fea_plan_missing_entry": (c_int, [c_void_p, _P64, _P64, _P64]),

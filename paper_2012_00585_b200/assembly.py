@@ -213,6 +213,10 @@ class Plan:
                                            _ptr(values_host), flags, _stream_ptr(stream)))
         return values_host
 
+    def set_host_windows(self, n_windows: int) -> None:
+        """Pipeline depth of assemble_host (0 = automatic; see fea_plan_set_host_windows)."""
+        _check(self._lib.fea_plan_set_host_windows(self._h, int(n_windows)))
+
     def assemble_host_batch(self, K_hosts, values_hosts, strategy: str = "sorted",
                             accumulate: bool = False, stream=None):
         """Pipelined repeated end-to-end assemblies: K_hosts[i] (host) -> values_hosts[i] (host).

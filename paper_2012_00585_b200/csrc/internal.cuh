@@ -56,6 +56,30 @@ struct DeviceScope {
     ~DeviceScope();
 };
 
+// Environment A/B switches of the numeric kernels, read once per process
+// instead of on every assembly.
+struct Knobs {
+    bool atomic_legacy, slot_no_fixed, cn_unpacked, cn_no_records, d1_no_direct, d1_no_vec;
+    int d1_acc_mod, d1v_acc_mod;  // accumulator stride residues (mod 16 doubles)
+};
+const Knobs& knobs();
+
+// Stream/event set of the end-to-end host paths (fea_assemble_host pipeline and
+// fea_assemble_host_batch), created on first use and kept with the plan.
+struct HostPipe {
+    cudaStream_t sin = nullptr, sout = nullptr;
+    std::vector<cudaEvent_t> ev;  // 2 per window (+1), 6 for the batch path
+    // fea_assemble_host windows: traversal windows [t_win[j], t_win[j+1]) and, per window, the
+    // K rows every window up to it needs (k_end, prefix max) and its values range (contiguous
+    // when nodes are traversed in id order)
+    int n_win = 0;
+    int32_t want_win = 0;  // fea_plan_set_host_windows (0: automatic)
+    std::vector<int64_t> t_win, k_end, v_off;
+    bool v_contiguous = false;
+    void ensure_events(int n);
+    ~HostPipe();
+};
+
 }  // namespace feagpu
 
 // The plan: everything the numeric phase needs, resolved once (north-star
@@ -133,6 +157,21 @@ struct fea_plan {
     bool slot_disabled = false;  // FEA_GATHER_NO_SLOT=1: column-node gather for d in 2..4 (A/B)
     feagpu::DevBuf stage_K, stage_V;       // fea_assemble_host staging
     feagpu::DevBuf bstage_K[2], bstage_V[2];  // fea_assemble_host_batch double buffers
+    feagpu::HostPipe pipe;                    // end-to-end streams, events, K/values windows
+    // launch bookkeeping that never changes for a plan (cached instead of queried per call)
+    int32_t sms = 0;  // SM count of the plan's device
+    struct Occ {
+        const void* fn;
+        size_t smem;
+        int threads, per_sm;
+    };
+    std::vector<Occ> occ_cache;
+    // traversal window of the gather launch: nodes [win_t0, win_t0 + win_n) of the traversal
+    // order (the fea_assemble_host pipeline runs one window per K chunk); win_n < 0: all.
+    // win_query: the launcher only reports (win_ok) whether its kernel takes windows, after
+    // building its lazy tables, and launches nothing.
+    int64_t win_t0 = 0, win_n = -1;
+    bool win_query = false, win_ok = false;
     int64_t kbytes_required() const;
     int64_t krows() const { return k_compact ? E : E_in; }
 };

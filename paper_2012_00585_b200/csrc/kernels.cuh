@@ -5,6 +5,7 @@
 #include <cub/cub.cuh>
 
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "internal.cuh"
@@ -1769,6 +1770,52 @@ void cub_call(F&& f) {
 
 // --- launch helpers --------------------------------------------------------
 
+// Per (plan, kernel, block size, shared memory): raise the kernel's dynamic shared-memory
+// limit if needed and return its resident CTAs per SM. Cached in the plan, so a repeated
+// assembly does no attribute or occupancy queries (host latency on small meshes).
+template <class F>
+int launch_prep(fea_plan* p, F* kern, int threads, size_t smem) {
+    const void* fn = reinterpret_cast<const void*>(kern);
+    for (const auto& c : p->occ_cache)
+        if (c.fn == fn && c.smem == smem && c.threads == threads) return c.per_sm;
+    if (smem > 48 * 1024) {
+        // the attribute is per kernel and process-wide: only ever raise it (another plan may
+        // need more than this one)
+        static std::mutex mu;
+        static std::vector<std::pair<std::pair<const void*, int>, size_t>> limit;
+        std::lock_guard<std::mutex> lk(mu);
+        size_t* cur = nullptr;
+        for (auto& l : limit)
+            if (l.first.first == fn && l.first.second == p->device) cur = &l.second;
+        if (!cur || *cur < smem) {
+            FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            if (cur) *cur = smem;
+            else limit.push_back({{fn, p->device}, smem});
+        }
+    }
+    int per_sm = 0;
+    FEA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+    p->occ_cache.push_back({fn, smem, threads, per_sm});
+    return per_sm;
+}
+
+// Traversal window of a windowed gather launch (fea_plan::win_t0 / win_n).
+struct Win {
+    int64_t t0, n;
+};
+inline Win window_of(const fea_plan* p) {
+    return p->win_n >= 0 ? Win{p->win_t0, p->win_n} : Win{0, p->n_own};
+}
+// Launchers whose kernel does not take windows: report it to a query, refuse a window.
+inline bool no_window(fea_plan* p) {
+    if (p->win_query) {
+        p->win_ok = false;
+        return true;
+    }
+    FEA_REQUIRE(p->win_n < 0, FEA_ERR_INVALID, "internal: traversal window on a kernel without windows");
+    return false;
+}
+
 GenK gen_of(const fea_plan* p) {
     GenK g{};
     g.on = p->gen_on ? 1 : 0;
@@ -1791,11 +1838,9 @@ void run_gather_stream(fea_plan* p, const Incidences& in, const double* K, doubl
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID,
                 "node row block too large for shared-memory accumulation");
     auto kern = p->dup_nodes ? k_gather_stream<G, R, PF, PosT, false> : k_gather_stream<G, R, PF, PosT, true>;
-    FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0, n_sm = 0;
-    FEA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kWarps * 32, smem));
-    FEA_CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, p->device));
-    if (p->n_own == 0) return;
+    const int occ = launch_prep(p, kern, kWarps * 32, smem);
+    const int n_sm = p->sms;
+    if (no_window(p) || p->n_own == 0) return;
     // persistent: one wave of CTAs, each group a contiguous node range (>= 2 nodes per group)
     int64_t blocks = static_cast<int64_t>(std::max(occ, 1)) * n_sm;
     blocks = std::min<int64_t>(blocks, (p->n_own + 2 * kWarps * GPW - 1) / (2 * kWarps * GPW));
@@ -1822,8 +1867,8 @@ void run_gather_node(fea_plan* p, const Incidences& in, const double* K, double*
                                           : k_gather_node<G, R, PF, PosT, true, true>)
                           : (p->dup_nodes ? k_gather_node<G, R, PF, PosT, false, false>
                                           : k_gather_node<G, R, PF, PosT, true, false>);
-    if (smem > 48 * 1024)
-        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    launch_prep(p, kern, kWarps * 32, smem);
+    if (no_window(p)) return;
     const int64_t groups = p->n_own;
     const int64_t blocks = (groups + kWarps * GPW - 1) / (kWarps * GPW);
     if (blocks == 0) return;
@@ -1864,7 +1909,7 @@ void run_gather_slot(fea_plan* p, const Incidences& in, const double* K, double*
     const bool sorted_inc = in.adj == p->adj.as<int32_t>();
     feagpu::DevBuf& fx = sorted_inc ? p->slot_rec : p->slot_recC;
     const bool fixed = !p->gen_on && (sorted_inc || in.adj == p->adjC.as<int32_t>()) &&
-                       !std::getenv("FEA_SLOT_NO_FIXED") && (fx.p || !capturing(s));
+                       !knobs().slot_no_fixed && (fx.p || !capturing(s));
     if (fixed && !fx.p) {
         if (!p->slot_hdr.p) p->slot_hdr.alloc(std::max<int64_t>(p->n_own, 1) * 16);
         fx.alloc(std::max<int64_t>(p->n_own, 1) * nbuf * 16);
@@ -1877,19 +1922,23 @@ void run_gather_slot(fea_plan* p, const Incidences& in, const double* K, double*
     auto kern = fixed ? (p->dup_nodes ? k_gather_slot<D, NPE, false, false, true> : k_gather_slot<D, NPE, true, false, true>)
                 : p->gen_on ? (p->dup_nodes ? k_gather_slot<D, NPE, false, true, false> : k_gather_slot<D, NPE, true, true, false>)
                           : (p->dup_nodes ? k_gather_slot<D, NPE, false, false, false> : k_gather_slot<D, NPE, true, false, false>);
-    if (smem > 48 * 1024)
-        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int dev = 0, sms = 148, per_sm = 1;
-    FEA_CK(cudaGetDevice(&dev));
-    FEA_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    FEA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSlotWarps * 32, smem));
-    const int64_t want = (p->n_own + kSlotWarps - 1) / kSlotWarps;  // one node per warp at most
-    const int64_t blocks = std::min<int64_t>(want, static_cast<int64_t>(sms) * std::max(per_sm, 1));
+    const int per_sm = launch_prep(p, kern, kSlotWarps * 32, smem);
+    if (p->win_query) {
+        p->win_ok = true;
+        return;
+    }
+    // window: shift the per-traversal-position arrays (order, fixed tables; without an order
+    // the node id is the position, so adj_ptr / nptr shift instead)
+    const Win wn = window_of(p);
+    const int32_t* order = p->node_order.p ? p->node_order.as<int32_t>() + wn.t0 : nullptr;
+    const int64_t shift = order ? 0 : wn.t0;
+    const int64_t want = (wn.n + kSlotWarps - 1) / kSlotWarps;  // one node per warp at most
+    const int64_t blocks = std::min<int64_t>(want, static_cast<int64_t>(p->sms) * std::max(per_sm, 1));
     if (blocks == 0) return;
     kern<<<static_cast<unsigned>(blocks), kSlotWarps * 32, smem, s>>>(
-        K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const uint8_t*>(in.posA), p->nptr.as<int64_t>(),
-        p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, nbuf, istr, accumulate ? 1 : 0,
-        gen_of(p), fixed ? p->slot_hdr.as<int4>() : nullptr, fixed ? fx.as<int4>() : nullptr, values);
+        K, p->adj_ptr.as<int64_t>() + shift, in.adj, static_cast<const uint8_t*>(in.posA),
+        p->nptr.as<int64_t>() + shift, order, wn.n, nbuf, istr, accumulate ? 1 : 0, gen_of(p),
+        fixed ? p->slot_hdr.as<int4>() + wn.t0 : nullptr, fixed ? fx.as<int4>() + wn.t0 * nbuf : nullptr, values);
     FEA_CK(cudaGetLastError());
     p->last_launches += 1;
 }
@@ -1927,7 +1976,7 @@ __global__ void k_cta_acc_max(const int32_t* __restrict__ order, const int64_t* 
 }
 
 int64_t cn_cta_acc(fea_plan* p, int per_cta, cudaStream_t s) {
-    if (std::getenv("FEA_CN_UNPACKED")) return static_cast<int64_t>(per_cta) * (p->d * p->d * p->max_cnt + 1);
+    if (knobs().cn_unpacked) return static_cast<int64_t>(per_cta) * (p->d * p->d * p->max_cnt + 1);
     if (p->cn_cta_acc > 0 && p->cn_cta_per == per_cta) return p->cn_cta_acc;
     DevBuf out;
     out.alloc(8);
@@ -1958,7 +2007,7 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
     if (G == 32 && sizeof(PosT) == 1 && !p->dup_nodes && p->max_adj <= kCnrSlots &&
         p->npe <= kCnrBytes - 4 && (in.adj == p->adj.as<int32_t>() || in.adj == p->adjC.as<int32_t>()) &&
-        !std::getenv("FEA_CN_NO_RECORDS") &&
+        !knobs().cn_no_records &&
         ((p->cnr_hdr.p && (in.adj == p->adj.as<int32_t>() ? p->cnr_rec.p : p->cnr_recC.p)) || !capturing(s))) {
         // built lazily on the first assembly of each incidence order: 16 + 256 bytes per node
         feagpu::DevBuf& recs = in.adj == p->adj.as<int32_t>() ? p->cnr_rec : p->cnr_recC;
@@ -1976,13 +2025,20 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
         const size_t smem_r = static_cast<size_t>(cta_acc) * sizeof(double) + kWarps * kCnrSlots * kCnrBytes;
         FEA_REQUIRE(smem_r <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
         auto kr = p->gen_on ? k_gather_cnr<D, FEA_CNR_PF, true> : k_gather_cnr<D, FEA_CNR_PF, false>;
-        if (smem_r > 48 * 1024)
-            FEA_CK(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
-        const int64_t blocks_r = (p->n_own + kWarps - 1) / kWarps;
+        launch_prep(p, kr, kWarps * 32, smem_r);
+        if (p->win_query) {
+            p->win_ok = true;
+            return;
+        }
+        // windows start at multiples of kWarps (the headers' packed accumulator offsets are
+        // relative to CTAs of kWarps consecutive traversal positions)
+        const Win wn = window_of(p);
+        FEA_REQUIRE(wn.t0 % kWarps == 0, FEA_ERR_INVALID, "internal: window not CTA-aligned");
+        const int64_t blocks_r = (wn.n + kWarps - 1) / kWarps;
         if (blocks_r == 0) return;
         kr<<<static_cast<unsigned>(blocks_r), kWarps * 32, smem_r, s>>>(
-            K, p->cnr_hdr.as<int4>(), recs.as<int2>(), p->n_own, p->npe, accumulate ? 1 : 0, cta_acc, gen_of(p),
-            values);
+            K, p->cnr_hdr.as<int4>() + wn.t0, recs.as<int2>() + wn.t0 * (kCnrSlots * kCnrBytes / 8), wn.n, p->npe,
+            accumulate ? 1 : 0, cta_acc, gen_of(p), values);
         FEA_CK(cudaGetLastError());
         p->last_launches += 1;
         return;
@@ -1991,8 +2047,8 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
                                           : k_gather_cn<G, D, PF, PosT, true, true>)
                           : (p->dup_nodes ? k_gather_cn<G, D, PF, PosT, false, false>
                                           : k_gather_cn<G, D, PF, PosT, true, false>);
-    if (smem > 48 * 1024)
-        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    launch_prep(p, kern, kWarps * 32, smem);
+    if (no_window(p)) return;
     const int64_t blocks = (p->n_own + kWarps * GPW - 1) / (kWarps * GPW);
     if (blocks == 0) return;
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
@@ -2011,7 +2067,7 @@ void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* v
     // (0.642 ms vs 0.664 at 15 and 0.670 at 1)
     int acc_stride = std::max(p->max_cnt, 1);
     int acc_mod = 3;
-    if (const char* e = std::getenv("FEA_D1_ACC_STRIDE_MOD16")) acc_mod = std::atoi(e) & 15;
+    if (knobs().d1_acc_mod >= 0) acc_mod = knobs().d1_acc_mod;
     while ((acc_stride & 15) != acc_mod) ++acc_stride;
     const int cap = static_cast<int>(std::max<int64_t>(p->max_adj, 1));
     const int pw = p->pstride * static_cast<int>(sizeof(PosT)) / 4;
@@ -2025,8 +2081,6 @@ void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* v
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
     auto kern = p->gen_on ? (p->dup_nodes ? k_gather_d1<G, PF, PosT, false, true> : k_gather_d1<G, PF, PosT, true, true>)
                           : (p->dup_nodes ? k_gather_d1<G, PF, PosT, false, false> : k_gather_d1<G, PF, PosT, true, false>);
-    if (smem > 48 * 1024)
-        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t per_cta = static_cast<int64_t>(kWarps) * GPW;
     const int64_t blocks = (p->n_own + per_cta - 1) / per_cta;
     if (blocks == 0) return;
@@ -2037,24 +2091,30 @@ void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* v
     // npe = 4 with traversal records: direct-record kernel for a materialized K, two-lane
     // kernel for the fused supplier
     if (G == 4 && p->npe == 4 && trav && rw == 2 && !p->dup_nodes && sizeof(PosT) == 1 && !p->gen_on &&
-        !std::getenv("FEA_D1_NO_DIRECT")) {
+        !knobs().d1_no_direct) {
         const size_t smemg = static_cast<size_t>(kWarps) * GPW * acc_stride * sizeof(double);
         auto kg = k_gather_d1g<FEA_D1G_U>;
-        if (smemg > 48 * 1024)
-            FEA_CK(cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemg));
-        kg<<<static_cast<unsigned>(blocks), kWarps * 32, smemg, s>>>(
-            K, p->n_own, acc_stride, accumulate ? 1 : 0, p->trav_ptr.as<int64_t>(), p->trav_meta.as<int64_t>(),
-            reinterpret_cast<const int2*>(recs.as<int32_t>()), values);
+        launch_prep(p, kg, kWarps * 32, smemg);
+        if (p->win_query) {
+            p->win_ok = true;
+            return;
+        }
+        const Win wn = window_of(p);
+        const int64_t blocks_w = (wn.n + per_cta - 1) / per_cta;
+        if (blocks_w == 0) return;
+        kg<<<static_cast<unsigned>(blocks_w), kWarps * 32, smemg, s>>>(
+            K, wn.n, acc_stride, accumulate ? 1 : 0, p->trav_ptr.as<int64_t>() + wn.t0,
+            p->trav_meta.as<int64_t>() + wn.t0, reinterpret_cast<const int2*>(recs.as<int32_t>()), values);
         FEA_CK(cudaGetLastError());
         p->last_launches += 1;
         return;
     }
     if (G == 4 && p->npe == 4 && trav && rw == 2 && !p->dup_nodes && sizeof(PosT) == 1 && p->gen_on &&
-        !std::getenv("FEA_D1_NO_VEC")) {
+        !knobs().d1_no_vec) {
         constexpr int GPW2 = 16;
         int acc_stride2 = std::max(p->max_cnt, 1);
         int acc_mod2 = 3;
-        if (const char* e = std::getenv("FEA_D1V_ACC_STRIDE_MOD16")) acc_mod2 = std::atoi(e) & 15;
+        if (knobs().d1v_acc_mod >= 0) acc_mod2 = knobs().d1v_acc_mod;
         while ((acc_stride2 & 15) != acc_mod2) ++acc_stride2;
         const size_t smem2 = static_cast<size_t>(kWarps) * GPW2 *
                              (acc_stride2 * sizeof(double) + static_cast<size_t>(rec_stride) * sizeof(int32_t));
@@ -2063,8 +2123,8 @@ void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* v
 #define FEA_D1V_PF 4
 #endif
         auto kern2 = k_gather_d1v<FEA_D1V_PF>;
-        if (smem2 > 48 * 1024)
-            FEA_CK(cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+        launch_prep(p, kern2, kWarps * 32, smem2);
+        if (no_window(p)) return;
         const int64_t per_cta2 = static_cast<int64_t>(kWarps) * GPW2;
         const int64_t blocks2 = (p->n_own + per_cta2 - 1) / per_cta2;
         if (blocks2 == 0) return;
@@ -2074,6 +2134,8 @@ void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* v
         p->last_launches += 1;
         return;
     }
+    launch_prep(p, kern, kWarps * 32, smem);
+    if (no_window(p)) return;
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
         K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const PosT*>(in.posA), p->nptr.as<int64_t>(),
         p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->n_own, p->npe, p->pstride, cap,
@@ -2149,8 +2211,7 @@ void run_scatter(fea_plan* p, const double* K, const int32_t* list, int64_t n_li
                         static_cast<size_t>(kWarps) * GPW * p->npe * (8 + 4);
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "element matrix too large for the scatter kernel");
     auto kern = k_scatter<G, PosT, ATOMIC>;
-    if (smem > 48 * 1024)
-        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    launch_prep(p, kern, kWarps * 32, smem);
     const int64_t blocks = std::min<int64_t>((n_list + kWarps * GPW - 1) / (kWarps * GPW), 148 * 16);
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
         K, list, n_list, p->elem_krow.as<int32_t>(), p->conn_k.as<int32_t>(), p->posE.as<PosT>(),
@@ -2177,11 +2238,8 @@ void run_atomic_staged(fea_plan* p, const double* K, double* values, cudaStream_
     if (n_steps == 0) return;
     const size_t smem = static_cast<size_t>(kWarps) * STAGES * S::STAGE;
     auto kern = k_atomic_staged<D, NPE, PosT, STAGES>;
-    if (smem > 48 * 1024)
-        FEA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0, sms = 0;
-    FEA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem));
-    FEA_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+    const int per_sm = launch_prep(p, kern, kWarps * 32, smem);
+    const int sms = p->sms;
     const int64_t blocks = std::min<int64_t>((n_steps + kWarps - 1) / kWarps,
                                              static_cast<int64_t>(sms) * std::max(per_sm, 1));
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
@@ -2195,9 +2253,8 @@ void run_atomic_cta(fea_plan* p, const double* K, double* values, cudaStream_t s
     const int64_t n_steps = p->at_E_pad;
     if (n_steps == 0) return;
     auto kern = k_atomic_direct<D, NPE, PosT>;
-    int per_sm = 0, sms = 0;
-    FEA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAtCtaThreads, 0));
-    FEA_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+    const int per_sm = launch_prep(p, kern, kAtCtaThreads, 0);
+    const int sms = p->sms;
     const int64_t blocks = std::min<int64_t>(n_steps, static_cast<int64_t>(sms) * std::max(per_sm, 1));
     kern<<<static_cast<unsigned>(blocks), kAtCtaThreads, 0, s>>>(
         K, p->at_krow.as<int32_t>(), p->at_rows.as<int64_t>(), p->at_pos.as<PosT>(), n_steps, values);

@@ -86,7 +86,7 @@ void ensure_element_maps(fea_plan* p, cudaStream_t s) {
 void build_atomic_maps(fea_plan* p, cudaStream_t s) {
     const bool shape = (p->d >= 1 && p->d <= 3 && (p->npe == 4 || p->npe == 8)) ||
                        ((p->d == 1 || p->d == 3) && p->npe == 27);  // k_atomic_staged / k_atomic_cta
-    if (!shape || p->E == 0 || std::getenv("FEA_ATOMIC_LEGACY") ||
+    if (!shape || p->E == 0 || knobs().atomic_legacy ||
         static_cast<int64_t>(p->d) * p->max_cnt >= (1 << 20))
         return;
     const int mm = p->m * p->m;
@@ -157,6 +157,173 @@ void assemble(fea_plan* p, const double* K, int strategy, double* values, uint32
     }
 }
 
+
+// --- end-to-end host path (fea_assemble_host) --------------------------------------------
+// The whole K must be on the device before the LAST node of the traversal can be assembled,
+// but a node needs only the element matrices of its incident elements. For meshes whose
+// element order follows the node order (structured meshes, z-slabs: config 5), the K rows
+// the first nodes need arrive first. The host path therefore splits the traversal into W
+// windows, uploads K in the chunks each window first needs (prefix max of its incidences'
+// K rows), launches window j as soon as its chunk has landed, and downloads window j's values
+// (a contiguous range when nodes are traversed in id order) while later chunks are still
+// coming in: host->device, kernels and device->host overlap, so one call costs about
+// max(K upload, values download) instead of their sum. Meshes without that locality (permuted
+// element order: window 0 already needs almost all of K) degrade to one upload, then the
+// windows, then the download.
+
+__global__ void k_window_tables(const int32_t* __restrict__ order, const int64_t* __restrict__ adj_ptr,
+                                const int32_t* __restrict__ adj, const int64_t* __restrict__ nptr,
+                                int64_t n_own, int npe, int64_t win, int n_win, int dd,
+                                unsigned long long* __restrict__ kmax, int64_t* __restrict__ voff) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i <= n_win) voff[i] = dd * nptr[i * win < n_own ? i * win : n_own];
+    for (int64_t t = i; t < n_own; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = order != nullptr ? order[t] : t;
+        int64_t mx = -1;
+        for (int64_t a = adj_ptr[v]; a < adj_ptr[v + 1]; ++a) mx = max(mx, static_cast<int64_t>(adj[a] / npe));
+        if (mx >= 0) atomicMax(kmax + t / win, static_cast<unsigned long long>(mx + 1));
+    }
+}
+
+void ensure_windows(fea_plan* p, cudaStream_t s) {
+    HostPipe& q = p->pipe;
+    if (q.n_win > 0) return;
+    const int64_t kb = p->kbytes_required();
+    // K chunks of >= 256 MB, at most 32 windows (or the caller's count), windows a multiple of
+    // 64 traversal positions
+    int64_t n_win = q.want_win > 0 ? q.want_win
+                                   : std::min<int64_t>(32, std::max<int64_t>(1, kb / (int64_t{256} << 20)));
+    int64_t win = (p->n_own + n_win - 1) / std::max<int64_t>(n_win, 1);
+    win = std::max<int64_t>(64, (win + 63) / 64 * 64);
+    n_win = std::max<int64_t>(1, (p->n_own + win - 1) / win);
+    q.n_win = static_cast<int>(n_win);
+    q.t_win.resize(n_win + 1);
+    for (int64_t j = 0; j <= n_win; ++j) q.t_win[j] = std::min<int64_t>(j * win, p->n_own);
+    q.k_end.assign(n_win, 0);
+    q.v_off.assign(n_win + 1, 0);
+    q.v_contiguous = p->node_order.p == nullptr;
+    if (p->n_own == 0) return;
+    DevBuf kmax, voff;
+    kmax.alloc(n_win * 8);
+    voff.alloc((n_win + 1) * 8);
+    FEA_CK(cudaMemsetAsync(kmax.p, 0, n_win * 8, s));
+    k_window_tables<<<grid_for(std::max<int64_t>(p->n_own, n_win + 1), 256), 256, 0, s>>>(
+        p->node_order.p ? p->node_order.as<int32_t>() : nullptr, p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(),
+        p->nptr.as<int64_t>(), p->n_own, p->npe, win, static_cast<int>(n_win), p->d * p->d,
+        kmax.as<unsigned long long>(), voff.as<int64_t>());
+    FEA_CK(cudaGetLastError());
+    std::vector<unsigned long long> hk(n_win);
+    FEA_CK(cudaMemcpyAsync(hk.data(), kmax.p, n_win * 8, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaMemcpyAsync(q.v_off.data(), voff.p, (n_win + 1) * 8, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaStreamSynchronize(s));
+    int64_t run = 0;
+    for (int64_t j = 0; j < n_win; ++j) {
+        run = std::max<int64_t>(run, static_cast<int64_t>(hk[j]));
+        q.k_end[j] = run;
+    }
+}
+
+void assemble_host_pipelined(fea_plan* p, const double* K_host, int32_t strategy, double* values_host,
+                             uint32_t flags, cudaStream_t sc) {
+    const size_t kb = static_cast<size_t>(p->kbytes_required());
+    const size_t vb = static_cast<size_t>(p->nnz) * 8;
+    FEA_REQUIRE(kb == 0 || K_host, FEA_ERR_INVALID, "K is NULL");
+    FEA_REQUIRE(vb == 0 || values_host, FEA_ERR_INVALID, "values is NULL");
+    if (p->stage_K.bytes < kb) p->stage_K.alloc(kb);
+    if (p->stage_V.bytes < vb) p->stage_V.alloc(vb);
+    double* dK = p->stage_K.as<double>();
+    double* dV = p->stage_V.as<double>();
+    const bool acc = !(flags & FEA_OVERWRITE);
+    HostPipe& q = p->pipe;
+    // windows only for the segmented-reduction routes whose kernel takes them (asked after the
+    // kernel's lazy tables are built: the query call launches nothing)
+    bool windows = false;
+    if (strategy == FEA_DET_SORTED || (strategy == FEA_DET_COLOUR && !(flags & FEA_COLOUR_PASSES))) {
+        ensure_windows(p, sc);
+        if (q.n_win > 1) {
+            p->win_query = true;
+            p->win_ok = false;
+            try {
+                assemble(p, dK, strategy, dV, flags, sc);
+            } catch (...) {
+                p->win_query = false;
+                throw;
+            }
+            p->win_query = false;
+            windows = p->win_ok;
+        }
+    }
+    const int nw = windows ? q.n_win : 1;
+    q.ensure_events(2 * nw + 1);
+    cudaEvent_t* ev_in = q.ev.data();
+    cudaEvent_t* ev_done = q.ev.data() + nw;
+    cudaEvent_t ev_start = q.ev[2 * nw];
+    FEA_CK(cudaEventRecord(ev_start, sc));  // copies start behind the caller's queued work
+    FEA_CK(cudaStreamWaitEvent(q.sin, ev_start, 0));
+    FEA_CK(cudaStreamWaitEvent(q.sout, ev_start, 0));
+    const int64_t mm = static_cast<int64_t>(p->m) * p->m;
+    int32_t launches = 0;
+    struct WinReset {
+        fea_plan* p;
+        ~WinReset() { p->win_n = -1; p->win_t0 = 0; }
+    } wr{p};
+    try {
+        if (!windows) {
+            if (kb) FEA_CK(cudaMemcpyAsync(dK, K_host, kb, cudaMemcpyHostToDevice, q.sin));
+            if (acc && vb) FEA_CK(cudaMemcpyAsync(dV, values_host, vb, cudaMemcpyHostToDevice, q.sin));
+            FEA_CK(cudaEventRecord(ev_in[0], q.sin));
+            FEA_CK(cudaStreamWaitEvent(sc, ev_in[0], 0));
+            assemble(p, dK, strategy, dV, flags, sc);
+            launches = p->last_launches;
+            FEA_CK(cudaEventRecord(ev_done[0], sc));
+            FEA_CK(cudaStreamWaitEvent(q.sout, ev_done[0], 0));
+            if (vb) FEA_CK(cudaMemcpyAsync(values_host, dV, vb, cudaMemcpyDeviceToHost, q.sout));
+        } else {
+            const bool vc = q.v_contiguous;
+            if (acc && !vc && vb) FEA_CK(cudaMemcpyAsync(dV, values_host, vb, cudaMemcpyHostToDevice, q.sin));
+            int64_t k_done = 0;
+            for (int j = 0; j < nw; ++j) {
+                const int64_t k_hi = q.k_end[j];
+                if (k_hi > k_done) {
+                    FEA_CK(cudaMemcpyAsync(dK + k_done * mm, K_host + k_done * mm,
+                                           static_cast<size_t>(k_hi - k_done) * mm * 8, cudaMemcpyHostToDevice,
+                                           q.sin));
+                    k_done = k_hi;
+                }
+                const int64_t v0 = q.v_off[j], v1 = q.v_off[j + 1];
+                if (acc && vc && v1 > v0)
+                    FEA_CK(cudaMemcpyAsync(dV + v0, values_host + v0, (v1 - v0) * 8, cudaMemcpyHostToDevice, q.sin));
+                FEA_CK(cudaEventRecord(ev_in[j], q.sin));
+                FEA_CK(cudaStreamWaitEvent(sc, ev_in[j], 0));
+                p->win_t0 = q.t_win[j];
+                p->win_n = q.t_win[j + 1] - q.t_win[j];
+                assemble(p, dK, strategy, dV, flags, sc);
+                launches += p->last_launches;
+                FEA_CK(cudaEventRecord(ev_done[j], sc));
+                if (vc && v1 > v0) {
+                    FEA_CK(cudaStreamWaitEvent(q.sout, ev_done[j], 0));
+                    FEA_CK(cudaMemcpyAsync(values_host + v0, dV + v0, (v1 - v0) * 8, cudaMemcpyDeviceToHost, q.sout));
+                }
+            }
+            p->win_n = -1;
+            p->win_t0 = 0;
+            if (!vc && vb) {
+                FEA_CK(cudaStreamWaitEvent(q.sout, ev_done[nw - 1], 0));
+                FEA_CK(cudaMemcpyAsync(values_host, dV, vb, cudaMemcpyDeviceToHost, q.sout));
+            }
+        }
+        FEA_CK(cudaStreamSynchronize(q.sin));
+        FEA_CK(cudaStreamSynchronize(sc));
+        FEA_CK(cudaStreamSynchronize(q.sout));
+    } catch (...) {
+        cudaStreamSynchronize(q.sin);
+        cudaStreamSynchronize(sc);
+        cudaStreamSynchronize(q.sout);
+        throw;
+    }
+    p->last_launches = launches;
+}
+
 }  // namespace feagpu
 
 using namespace feagpu;
@@ -194,17 +361,7 @@ fea_status fea_assemble_host(fea_plan* plan, const double* K_host, int32_t strat
     return guarded_n([&] {
         FEA_REQUIRE(plan, FEA_ERR_INVALID, "plan is NULL");
         DeviceScope ds(plan->device);
-        cudaStream_t s = static_cast<cudaStream_t>(stream);
-        const size_t kb = static_cast<size_t>(plan->kbytes_required());
-        const size_t vb = static_cast<size_t>(plan->nnz) * 8;
-        if (plan->stage_K.bytes < kb) plan->stage_K.alloc(kb);
-        if (plan->stage_V.bytes < vb) plan->stage_V.alloc(vb);
-        if (kb) FEA_CK(cudaMemcpyAsync(plan->stage_K.p, K_host, kb, cudaMemcpyHostToDevice, s));
-        if (!(flags & FEA_OVERWRITE) && vb)
-            FEA_CK(cudaMemcpyAsync(plan->stage_V.p, values_host, vb, cudaMemcpyHostToDevice, s));
-        assemble(plan, plan->stage_K.as<double>(), strategy, plan->stage_V.as<double>(), flags, s);
-        if (vb) FEA_CK(cudaMemcpyAsync(values_host, plan->stage_V.p, vb, cudaMemcpyDeviceToHost, s));
-        FEA_CK(cudaStreamSynchronize(s));
+        assemble_host_pipelined(plan, K_host, strategy, values_host, flags, static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -226,15 +383,16 @@ fea_status fea_assemble_host_batch(fea_plan* plan, const double* const* K_hosts,
             if (plan->bstage_K[s2].bytes < kb) plan->bstage_K[s2].alloc(kb);
             if (plan->bstage_V[s2].bytes < vb) plan->bstage_V[s2].alloc(vb);
         }
-        cudaStream_t sin = nullptr, sout = nullptr;
-        FEA_CK(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
-        FEA_CK(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
-        cudaEvent_t ev_in[2], ev_done[2], ev_out[2];
-        for (int s2 = 0; s2 < 2; ++s2) {
-            FEA_CK(cudaEventCreateWithFlags(&ev_in[s2], cudaEventDisableTiming));
-            FEA_CK(cudaEventCreateWithFlags(&ev_done[s2], cudaEventDisableTiming));
-            FEA_CK(cudaEventCreateWithFlags(&ev_out[s2], cudaEventDisableTiming));
-        }
+        HostPipe& q = plan->pipe;
+        q.ensure_events(6);
+        cudaStream_t sin = q.sin, sout = q.sout;
+        cudaEvent_t* ev_in = q.ev.data();
+        cudaEvent_t* ev_done = q.ev.data() + 2;
+        cudaEvent_t* ev_out = q.ev.data() + 4;
+        // the copy streams start behind whatever the caller queued on its stream
+        FEA_CK(cudaEventRecord(ev_done[0], sc));
+        FEA_CK(cudaStreamWaitEvent(sin, ev_done[0], 0));
+        FEA_CK(cudaStreamWaitEvent(sout, ev_done[0], 0));
         int32_t launches = 0;
         try {
             for (int32_t i = 0; i < n_steps; ++i) {
@@ -264,19 +422,17 @@ fea_status fea_assemble_host_batch(fea_plan* plan, const double* const* K_hosts,
             cudaStreamSynchronize(sin);
             cudaStreamSynchronize(sc);
             cudaStreamSynchronize(sout);
-            for (int s2 = 0; s2 < 2; ++s2) {
-                cudaEventDestroy(ev_in[s2]); cudaEventDestroy(ev_done[s2]); cudaEventDestroy(ev_out[s2]);
-            }
-            cudaStreamDestroy(sin);
-            cudaStreamDestroy(sout);
             throw;
         }
-        for (int s2 = 0; s2 < 2; ++s2) {
-            cudaEventDestroy(ev_in[s2]); cudaEventDestroy(ev_done[s2]); cudaEventDestroy(ev_out[s2]);
-        }
-        cudaStreamDestroy(sin);
-        cudaStreamDestroy(sout);
         plan->last_launches = launches;
+    });
+}
+
+fea_status fea_plan_set_host_windows(fea_plan* plan, int32_t n_windows) {
+    return guarded_n([&] {
+        FEA_REQUIRE(plan && n_windows >= 0, FEA_ERR_INVALID, "bad arguments");
+        plan->pipe.want_win = n_windows;
+        plan->pipe.n_win = 0;  // rebuilt on the next fea_assemble_host
     });
 }
 

@@ -60,6 +60,40 @@ DeviceScope::~DeviceScope() {
     if (prev >= 0 && cur != prev) cudaSetDevice(prev);
 }
 
+const Knobs& knobs() {
+    static const Knobs k = [] {
+        auto on = [](const char* n) { return std::getenv(n) != nullptr; };
+        auto mod = [](const char* n) {
+            const char* e = std::getenv(n);
+            return e ? (std::atoi(e) & 15) : -1;
+        };
+        return Knobs{on("FEA_ATOMIC_LEGACY"), on("FEA_SLOT_NO_FIXED"),   on("FEA_CN_UNPACKED"),
+                     on("FEA_CN_NO_RECORDS"), on("FEA_D1_NO_DIRECT"),    on("FEA_D1_NO_VEC"),
+                     mod("FEA_D1_ACC_STRIDE_MOD16"), mod("FEA_D1V_ACC_STRIDE_MOD16")};
+    }();
+    return k;
+}
+
+void HostPipe::ensure_events(int n) {
+    if (!sin) {
+        FEA_CK(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
+        FEA_CK(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
+    }
+    while (static_cast<int>(ev.size()) < n) {
+        cudaEvent_t e = nullptr;
+        FEA_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ev.push_back(e);
+    }
+}
+
+HostPipe::~HostPipe() {
+    if (sin) cudaStreamSynchronize(sin);
+    if (sout) cudaStreamSynchronize(sout);
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (sin) cudaStreamDestroy(sin);
+    if (sout) cudaStreamDestroy(sout);
+}
+
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
@@ -1118,6 +1152,7 @@ fea_status fea_plan_create(int device, const int64_t* elem_dofs, int64_t n_eleme
         Stream st;
         auto p = std::make_unique<fea_plan>();
         p->device = device;
+        FEA_CK(cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device));
         p->cn_disabled = std::getenv("FEA_GATHER_NO_CN") != nullptr;
         p->d1_disabled = std::getenv("FEA_GATHER_NO_D1") != nullptr;
         p->slot_disabled = std::getenv("FEA_GATHER_NO_SLOT") != nullptr;
@@ -1189,6 +1224,7 @@ fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, in
         }
         auto p = std::make_unique<fea_plan>();
         p->device = device;
+        FEA_CK(cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device));
         p->external = true;
         p->E_in = n_elements;
         p->m = m;

@@ -26,24 +26,28 @@ def run(args, env=None, timeout=900):
 @pytest.mark.timeout(600)
 def test_reference_arm_contract(ref_lib):
     """--impl reference: the reference library on the host cores, same workload and metric."""
-    d = run(["--impl", "reference", "--steps", "2", "--warmup", "1"])
+    d = run(["--impl", "reference", "--steps", "2", "--warmup", "1", "--size", "32", "--sample-layers", "4"])
     assert BASE_KEYS <= set(d)
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "entries/s"
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
+    # the reference's four methods with t_avg / t_min (bench.cpp:126-156, :223-224)
+    assert set(d["config"]["methods"]) == {"spin-vec/crac", "colour-vec/crac", "atomic/csr", "seq/csr"}
+    assert d["t_min_ms"] <= d["ms_per_step"]
 
 
 @pytest.mark.gpu
 @pytest.mark.timeout(900)
 def test_gpu_arm_contract(gpu):
-    d = run(["--steps", "3", "--warmup", "3", "--no-cpu-baseline"])
+    d = run(["--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--size", "48"])
     assert BASE_KEYS <= set(d)
     assert d["n_gpus"] == 1 and d["dtype"] == "f64" and d["higher_is_better"] is True
     r = d["roofline"]
     assert r["bound"] == "hbm" and 0 < r["frac"] < 1.2 and r["unit"] == "GB/s"
     assert d["gpu_launches"] == 3
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["e2e"]["values_equal_device_run"] is True
     assert d["clocks"]["sm_mhz"] is not None
 
 
@@ -52,11 +56,14 @@ def test_gpu_arm_contract(gpu):
 def test_two_rank_partitioned_bench_matches_single_gpu(gpu):
     """torchrun, 2 ranks over gloo sharing the box's GPU: the row-partitioned path end to end;
     the gathered row blocks equal a single-GPU assembly of the global mesh bit for bit."""
-    d = run(["--gpus", "2", "--steps", "2", "--warmup", "3", "--gather", "--check", "--no-e2e"],
-            env={"FEA_BENCH_BACKEND": "gloo", "MASTER_PORT": "29541"})
+    d = run(["--gpus", "2", "--steps", "2", "--warmup", "3", "--gather", "--check", "--size", "16",
+             "--e2e-steps", "1"], env={"FEA_BENCH_BACKEND": "gloo", "MASTER_PORT": "29541"})
     assert d["n_gpus"] == 2 and d["gather"]["bitwise_equal_to_single_gpu"] is True
+    assert d["scaling"] == "strong" and d["config"]["redundant_element_fraction"] > 0
+    # every rank's host-path values equal its device-path values bit for bit
+    assert d["e2e"]["values_equal_device_run"] is True
     # the fused path (each rank assembles into rank 0's buffer through a CUDA IPC mapping)
-    assert d["gather"]["fused_assembly_into_root"]["equal_to_nccl_gather"] is True
+    assert d["gather"]["fused_equal_to_nccl_gather"] is True
 
 
 @pytest.mark.gpu

@@ -231,6 +231,32 @@ def test_host_end_to_end(gpu, orc):
         assert got.tobytes() == want.tobytes()
 
 
+@pytest.mark.parametrize("mesh,n,d,perm", [("hex8", 6, 3, None), ("hex8", 5, 3, "elements"),
+                                            ("tet4", 5, 1, "nodes"), ("quad4", 16, 1, None),
+                                            ("hex27", 3, 3, None), ("hex8", 5, 1, None), ("quad4", 9, 5, None)])
+@pytest.mark.parametrize("windows", [1, 5, 13])
+def test_host_windowed_pipeline(gpu, orc, mesh, n, d, perm, windows):
+    """fea_assemble_host in traversal windows (K chunks uploaded as windows need them, each
+    window's values downloaded as it completes): bit-exact vs assemble_sequential /
+    assemble_coloured_vectorized, overwrite and accumulate; atomic within 1e-12."""
+    conn, nn, ed, n_rows = problem(mesh, n, d, perm)
+    P = orc.Pattern.build(conn, nn, d)
+    Kh = orc.fill_k(7, conn.shape[0], ed.shape[1])
+    want = P.assemble_sequential(ed, Kh)
+    col, _ = orc.greedy_colouring(conn, nn)
+    want_c = P.assemble_coloured(ed, Kh, col)
+    with gpu.Plan(ed, n_rows, dofs_per_node=d) as plan:
+        plan.set_host_windows(windows)
+        plan.set_colouring(plan.greedy_colouring()[0])
+        for rep in range(2):  # second call reuses staging, streams and window tables
+            assert plan.assemble_host(Kh, strategy="sorted").tobytes() == want.tobytes()
+        assert plan.assemble_host(Kh, strategy="colour").tobytes() == want_c.tobytes()
+        start = np.full(P.nnz, 0.25)
+        got = plan.assemble_host(Kh, start.copy(), strategy="sorted", accumulate=True)
+        assert got.tobytes() == P.assemble_sequential(ed, Kh, start.copy()).tobytes()
+        assert close(plan.assemble_host(Kh, strategy="atomic"), want)
+
+
 def test_empty_and_degenerate(gpu):
     """test_formats.cpp:111-139: empty pattern / empty rows."""
     import torch

@@ -64,10 +64,15 @@ def test_kept_elements_and_halo():
     assert 0 < dist.redundant_fraction(conn, nn, 2) < 0.3
 
 
-def test_bench_owned_rows_cover_global_mesh():
+def test_bench_rank_node_ranges_cover_mesh_and_balance():
+    """bench.py --gpus N: contiguous node ranges covering the config-5 mesh (here at n=32),
+    cut at incidence quantiles: per-rank incidence counts within 2 % of each other."""
     import bench
+    conn, nn = M.hex8_structured(32)
+    w = np.bincount(conn.ravel(), minlength=nn)
     for N in (1, 2, 4, 8):
-        conn, nn = M.hex8_box(bench.NXY, bench.NXY, bench.NZ_PER_GPU * N)
-        ranges = [bench.owned_rows(N, r) for r in range(N)]
-        assert ranges[0][0] == 0 and ranges[-1][1] == nn * bench.D
+        ranges = [bench.rank_nodes(conn, nn, N, r) for r in range(N)]
+        assert ranges[0][0] == 0 and ranges[-1][1] == nn
         assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+        loads = [w[lo:hi].sum() for lo, hi in ranges]
+        assert max(loads) <= 1.02 * min(loads)
