@@ -136,11 +136,13 @@ FEA_API fea_status fea_plan_info(const fea_plan* plan, int32_t* dofs_per_node, i
                          int64_t* metadata_bytes);
 
 /* CSR arrays of the plan (SparsityPattern::row_ptr/cols, pattern.hpp:29-35):
- * row_ptr[n_rows+1], cols[nnz]; host or device destinations. */
+ * row_ptr[n_rows+1], cols[nnz]; host or device destinations (device ones are written in
+ * place); cols may be NULL to fetch only row_ptr. */
 FEA_API fea_status fea_plan_copy_csr(const fea_plan* plan, int64_t* row_ptr, int64_t* cols);
 
 /* CRAC arrays (CracBase::rows / col_align, formats.hpp:257-273): row_ptr[n_rows+1]
- * in col_align entry units, col_align[2*runs+2] with the final (0, nnz) pair. */
+ * in col_align entry units, col_align[2*runs+2] with the final (0, nnz) pair; host or
+ * device destinations; col_align may be NULL to fetch only row_ptr. */
 FEA_API fea_status fea_plan_copy_crac(const fea_plan* plan, int64_t* row_ptr, int64_t* col_align);
 
 /* Ids (ascending) of the elements the plan keeps (those with a node in the owned

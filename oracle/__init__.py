@@ -73,6 +73,13 @@ def orc():
         L.orc_assemble_coloured.restype = c_int
         L.orc_assemble_coloured.argtypes = [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p,
                                             c_void_p, c_void_p]
+        L.orc_adjacency_new.restype = c_void_p
+        L.orc_adjacency_new.argtypes = [c_void_p, c_int64, c_int, c_int64]
+        L.orc_adjacency_free.argtypes = [c_void_p]
+        L.orc_node_counts.argtypes = [c_void_p, c_int64, c_int64, c_void_p, c_void_p]
+        L.orc_node_rows.restype = c_int
+        L.orc_node_rows.argtypes = [c_void_p, c_int, c_uint64, c_void_p, c_void_p, c_int64, c_int, c_void_p,
+                                    c_void_p, c_void_p]
         _orc = L
     return _orc
 
@@ -143,6 +150,61 @@ class Pattern:
         try:
             if self._h:
                 orc().orc_pattern_free(self._h)
+        except Exception:
+            pass
+
+
+class Adjacency:
+    """Restricted oracle for meshes too large for the full one (SURVEY.md §8c "oracle limits",
+    config 5): the reference's node -> element index (pattern.cpp:32-48), node row lengths
+    (so the whole int64 row_ptr is checked) and the assembled values of selected node rows
+    with the seeded supplier (orc_node_rows: assemble_sequential / colour-vec order)."""
+
+    def __init__(self, conn: np.ndarray, n_nodes: int):
+        self._conn = np.ascontiguousarray(conn, dtype=np.int64)  # borrowed by the C side
+        self.n_nodes = n_nodes
+        self.npe = self._conn.shape[1]
+        self._h = c_void_p(orc().orc_adjacency_new(_p(self._conn), self._conn.shape[0], self.npe, n_nodes))
+
+    def node_counts(self, threads: int = 0):
+        """(count, runs) per node: node-level row length and CRAC runs."""
+        out = np.empty(self.n_nodes, np.int64)
+        runs = np.empty(self.n_nodes, np.int64)
+        threads = threads or (os.cpu_count() or 1)
+        step = max(1 << 14, (self.n_nodes + threads - 1) // threads)
+        L = orc()
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda v0: L.orc_node_counts(self._h, v0, min(v0 + step, self.n_nodes),
+                                                     c_void_p(out[v0:].ctypes.data), c_void_p(runs[v0:].ctypes.data)),
+                        range(0, self.n_nodes, step)))
+        return out, runs
+
+    def row_ptrs(self, d: int, threads: int = 0):
+        """Whole-matrix (CSR row_ptr, CRAC row_ptr) int64: row (v,k) has d*count(v) entries and
+        2*runs(v) col_align entries (build_crac_arrays, formats.cpp:21-41)."""
+        c, r = self.node_counts(threads)
+        rp = np.zeros(self.n_nodes * d + 1, np.int64)
+        rp[1:] = np.cumsum(np.repeat(c * d, d))
+        cp = np.zeros(self.n_nodes * d + 1, np.int64)
+        cp[1:] = np.cumsum(np.repeat(2 * r, d))
+        return rp, cp
+
+    def node_rows(self, nodes, d: int, seed: int, colour_of=None, max_cols: int = 128):
+        """(cnt[n], cols[n, max_cols] node ids, vals[n, d, max_cols*d]) of the selected nodes."""
+        nd = np.ascontiguousarray(nodes, dtype=np.int64)
+        cnt = np.zeros(len(nd), np.int64)
+        cols = np.zeros((len(nd), max_cols), np.int64)
+        vals = np.zeros((len(nd), d, max_cols * d), np.float64)
+        col = None if colour_of is None else np.ascontiguousarray(colour_of, dtype=np.int32)
+        if orc().orc_node_rows(self._h, d, seed, _p(col), _p(nd), len(nd), max_cols, _p(cnt), _p(cols), _p(vals)):
+            raise ValueError("node row longer than max_cols")
+        return cnt, cols, vals
+
+    def __del__(self):
+        try:
+            if self._h:
+                orc().orc_adjacency_free(self._h)
         except Exception:
             pass
 

@@ -359,3 +359,136 @@ int orc_assemble_coloured(const orc_pattern* p, const idx_t* elem_dofs, idx_t n_
         }
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Restricted oracle for sizes the full oracle cannot hold (SURVEY §8c,      */
+/* "oracle limits": config 5 has NNZ 4.09e9)                                 */
+/* ------------------------------------------------------------------------ */
+
+/* The node -> element inverted index of build_pattern (pattern.cpp:32-48), kept so that
+ * row counts and selected rows can be computed from several threads. element_nodes is
+ * borrowed (the caller keeps it alive). */
+typedef struct {
+    const idx_t* en;
+    idx_t n_elements, n_nodes;
+    int npe;
+    idx_t* adj_ptr;
+    idx_t* adj;
+} orc_adjacency;
+
+orc_adjacency* orc_adjacency_new(const idx_t* element_nodes, idx_t n_elements, int npe, idx_t n_nodes) {
+    orc_adjacency* a = (orc_adjacency*)calloc(1, sizeof(orc_adjacency));
+    a->en = element_nodes;
+    a->n_elements = n_elements;
+    a->n_nodes = n_nodes;
+    a->npe = npe;
+    node_adjacency(element_nodes, n_elements, npe, n_nodes, &a->adj_ptr, &a->adj);
+    return a;
+}
+
+void orc_adjacency_free(orc_adjacency* a) {
+    if (!a) return;
+    free(a->adj_ptr);
+    free(a->adj);
+    free(a);
+}
+
+/* sorted distinct neighbour nodes of v (build_pattern's per-node gather + sort/unique,
+ * pattern.cpp:71-83, at node level: the DOF list is this list times d). */
+static idx_t node_neighbours(const orc_adjacency* a, idx_t v, idx_t* scratch) {
+    idx_t len = 0;
+    for (idx_t k = a->adj_ptr[v]; k < a->adj_ptr[v + 1]; ++k)
+        for (int b = 0; b < a->npe; ++b) scratch[len++] = a->en[a->adj[k] * a->npe + b];
+    return sort_unique(scratch, len);
+}
+
+static idx_t max_degree(const orc_adjacency* a) {
+    idx_t mx = 0;
+    for (idx_t v = 0; v < a->n_nodes; ++v)
+        if (a->adj_ptr[v + 1] - a->adj_ptr[v] > mx) mx = a->adj_ptr[v + 1] - a->adj_ptr[v];
+    return mx;
+}
+
+/* Node-level row lengths and CRAC runs of nodes v0 .. v1-1, so the whole int64 CSR and CRAC
+ * row pointers follow by scans: row (v,k) has d * count(v) entries (pattern.cpp:85-95) and
+ * runs(v) maximal runs of consecutive columns (count_pattern_runs, pattern.cpp:110-120: with
+ * node-contiguous DOFs a run of consecutive DOFs is a run of consecutive nodes). */
+void orc_node_counts(const orc_adjacency* a, idx_t v0, idx_t v1, idx_t* out, idx_t* runs) {
+    idx_t* scratch = (idx_t*)malloc((size_t)(max_degree(a) * a->npe + 1) * sizeof(idx_t));
+    for (idx_t v = v0; v < v1; ++v) {
+        const idx_t c = node_neighbours(a, v, scratch);
+        out[v - v0] = c;
+        if (runs) {
+            idx_t r = 0;
+            for (idx_t i = 0; i < c; ++i)
+                if (i == 0 || scratch[i] != scratch[i - 1] + 1) ++r;
+            runs[v - v0] = r;
+        }
+    }
+    free(scratch);
+}
+
+/* The d rows of each selected node of the assembled matrix with the seeded supplier
+ * (orc_kval): sorted column nodes cols[i*max_cols ..] (cnt[i] of them) and values
+ * vals[(i*d + k) * max_cols*d + q] of row (v,k), slot q. Per slot the order of
+ * assemble_sequential (assembly.hpp:112-118: elements ascending, scatter_element row-major
+ * within an element, :77-92) or, with colour_of, of assemble_coloured_vectorized
+ * (assembly.hpp:175-195: colours ascending). Returns 0, or 1 if a row has > max_cols nodes. */
+int orc_node_rows(const orc_adjacency* a, int d, uint64_t seed, const int32_t* colour_of,
+                  const idx_t* nodes, idx_t n_sel, int max_cols, idx_t* cnt, idx_t* cols, double* vals) {
+    const int npe = a->npe, m = npe * d;
+    const idx_t deg = max_degree(a);
+    idx_t* scratch = (idx_t*)malloc((size_t)(deg * npe + 1) * sizeof(idx_t));
+    idx_t* elems = (idx_t*)malloc((size_t)(deg + 1) * sizeof(idx_t));
+    int rc = 0;
+    for (idx_t i = 0; i < n_sel && !rc; ++i) {
+        const idx_t v = nodes[i];
+        const idx_t c = node_neighbours(a, v, scratch);
+        if (c > max_cols) { rc = 1; break; }
+        cnt[i] = c;
+        memcpy(cols + i * max_cols, scratch, (size_t)c * sizeof(idx_t));
+        const idx_t rl = (idx_t)max_cols * d;
+        double* vrow = vals + i * d * rl;
+        for (idx_t q = 0; q < d * rl; ++q) vrow[q] = 0.0;
+        /* incident elements in summation order (ascending id; stable by colour) */
+        idx_t ne = 0;
+        for (idx_t k = a->adj_ptr[v]; k < a->adj_ptr[v + 1]; ++k)
+            if (ne == 0 || elems[ne - 1] != a->adj[k]) elems[ne++] = a->adj[k];
+        if (colour_of)
+            for (idx_t x = 1; x < ne; ++x) { /* insertion sort by colour, stable */
+                const idx_t e = elems[x];
+                idx_t y = x;
+                while (y > 0 && colour_of[elems[y - 1]] > colour_of[e]) { elems[y] = elems[y - 1]; --y; }
+                elems[y] = e;
+            }
+        for (idx_t x = 0; x < ne; ++x) {
+            const idx_t e = elems[x];
+            const idx_t* en = a->en + e * npe;
+            const uint64_t he = orc_splitmix64(seed + (uint64_t)e);
+            for (int ra = 0; ra < npe; ++ra) {
+                if (en[ra] != v) continue;
+                for (int k = 0; k < d; ++k) {
+                    const int r = ra * d + k;
+                    for (int cb = 0; cb < npe; ++cb) {
+                        /* position of column node en[cb] in the sorted list */
+                        idx_t lo = 0, hi = c;
+                        while (lo < hi) {
+                            const idx_t mid = (lo + hi) / 2;
+                            if (scratch[mid] < en[cb]) lo = mid + 1; else hi = mid;
+                        }
+                        for (int k2 = 0; k2 < d; ++k2) {
+                            const int cc = cb * d + k2;
+                            const uint64_t lo_ = (uint64_t)(r < cc ? r : cc), hi_ = (uint64_t)(r < cc ? cc : r);
+                            const uint64_t h = orc_splitmix64(he ^ ((lo_ << 32) | hi_));
+                            vrow[k * rl + lo * d + k2] += (double)(h >> 11) * 0x1p-53 * 2.0 - 1.0;
+                        }
+                    }
+                }
+            }
+        }
+        (void)m;
+    }
+    free(scratch);
+    free(elems);
+    return rc;
+}

@@ -131,6 +131,30 @@ class Plan:
         _check(self._lib.fea_plan_copy_csr(self._h, _ptr(row_ptr), _ptr(cols)))
         return row_ptr, cols[: self.nnz]
 
+    def row_ptr(self):
+        """CSR row_ptr only (host int64[n_rows+1])."""
+        row_ptr = np.empty(self.n_rows + 1, np.int64)
+        _check(self._lib.fea_plan_copy_csr(self._h, _ptr(row_ptr), c_void_p(0)))
+        return row_ptr
+
+    def csr_device(self):
+        """CSR arrays as device tensors (written in place: no host or device temporaries)."""
+        import torch
+        dev = f"cuda:{self.device}"
+        row_ptr = torch.empty(self.n_rows + 1, dtype=torch.int64, device=dev)
+        cols = torch.empty(max(self.nnz, 1), dtype=torch.int64, device=dev)
+        _check(self._lib.fea_plan_copy_csr(self._h, _ptr(row_ptr), _ptr(cols)))
+        return row_ptr, cols[: self.nnz]
+
+    def crac_device(self):
+        """CRAC arrays as device tensors."""
+        import torch
+        dev = f"cuda:{self.device}"
+        row_ptr = torch.empty(self.n_rows + 1, dtype=torch.int64, device=dev)
+        col_align = torch.empty(2 * self.n_runs + 2, dtype=torch.int64, device=dev)
+        _check(self._lib.fea_plan_copy_crac(self._h, _ptr(row_ptr), _ptr(col_align)))
+        return row_ptr, col_align
+
     def crac(self):
         row_ptr = np.empty(self.n_rows + 1, np.int64)
         col_align = np.empty(2 * self.n_runs + 2, np.int64)

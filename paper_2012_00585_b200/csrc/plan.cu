@@ -425,6 +425,7 @@ __global__ void k_expand_csr(const int64_t* __restrict__ nptr, const int32_t* __
         const int64_t rowlen = d * cnt;
         if (lane < d) row_ptr[v * d + lane] = base + lane * rowlen;
         if (v == n_own - 1 && lane == 0) row_ptr[n_own * d] = (int64_t)d * d * nptr[n_own];
+        if (cols == nullptr) continue;  // row pointers only
         const int32_t* list = ncol + nptr[v];
         for (int64_t i = lane; i < d * rowlen; i += 32) {
             const int64_t k = i / rowlen;
@@ -1338,48 +1339,65 @@ fea_status fea_plan_info(const fea_plan* p, int32_t* dofs_per_node, int32_t* nod
     });
 }
 
+// Device destinations are written in place (config 5's cols are 32.7 GB: no device temp);
+// cols / col_align may be NULL to fetch only the row pointers.
 fea_status fea_plan_copy_csr(const fea_plan* p, int64_t* row_ptr, int64_t* cols) {
     return guarded([&] {
-        FEA_REQUIRE(p && row_ptr && (p->nnz == 0 || cols), FEA_ERR_INVALID, "NULL argument");
+        FEA_REQUIRE(p && row_ptr, FEA_ERR_INVALID, "NULL argument");
         DeviceScope ds(p->device);
         Stream st;
         const int64_t rows = p->n_own * p->d;
         DevBuf drp, dcols;
-        drp.alloc((rows + 1) * 8);
-        dcols.alloc(p->nnz * 8);
-        FEA_CK(cudaMemsetAsync(drp.p, 0, 8, st.s));
+        int64_t* rp_d = row_ptr;
+        int64_t* cols_d = cols;
+        if (!is_device_ptr(row_ptr)) {
+            drp.alloc((rows + 1) * 8);
+            rp_d = drp.as<int64_t>();
+        }
+        if (cols && !is_device_ptr(cols)) {
+            dcols.alloc(p->nnz * 8);
+            cols_d = dcols.as<int64_t>();
+        }
+        FEA_CK(cudaMemsetAsync(rp_d, 0, 8, st.s));
         if (p->n_own > 0)
             k_expand_csr<<<grid_for(p->n_own * 32, 256), 256, 0, st.s>>>(
-                p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->n_own, p->d, p->node_begin,
-                drp.as<int64_t>(), dcols.as<int64_t>());
+                p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->n_own, p->d, p->node_begin, rp_d, cols_d);
         FEA_CK(cudaGetLastError());
-        copy_out(row_ptr, drp.p, (rows + 1) * 8, st.s);
-        copy_out(cols, dcols.p, p->nnz * 8, st.s);
+        if (drp.p) copy_out(row_ptr, drp.p, (rows + 1) * 8, st.s);
+        if (dcols.p) copy_out(cols, dcols.p, p->nnz * 8, st.s);
         FEA_CK(cudaStreamSynchronize(st.s));
     });
 }
 
 fea_status fea_plan_copy_crac(const fea_plan* p, int64_t* row_ptr, int64_t* col_align) {
     return guarded([&] {
-        FEA_REQUIRE(p && row_ptr && col_align, FEA_ERR_INVALID, "NULL argument");
+        FEA_REQUIRE(p && row_ptr, FEA_ERR_INVALID, "NULL argument");
         DeviceScope ds(p->device);
         Stream st;
         const int64_t rows = p->n_own * p->d;
         DevBuf dptr, dal;
-        dptr.alloc((rows + 1) * 8);
-        dal.alloc((2 * p->n_runs + 2) * 8);
+        int64_t* ptr_d = row_ptr;
+        int64_t* al_d = col_align;
+        if (!is_device_ptr(row_ptr)) {
+            dptr.alloc((rows + 1) * 8);
+            ptr_d = dptr.as<int64_t>();
+        }
+        if (!col_align || !is_device_ptr(col_align)) {  // the kernel always writes the pairs
+            dal.alloc((2 * p->n_runs + 2) * 8);
+            al_d = dal.as<int64_t>();
+        }
         if (p->n_own > 0) {
             k_expand_crac<<<grid_for(p->n_own, 128), 128, 0, st.s>>>(
                 p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->nrun_ptr.as<int64_t>(), p->n_own,
-                p->d, dptr.as<int64_t>(), dal.as<int64_t>());
+                p->d, ptr_d, al_d);
             FEA_CK(cudaGetLastError());
         } else {
             const int64_t z[2] = {0, 0};
-            FEA_CK(cudaMemcpyAsync(dptr.p, z, 8, cudaMemcpyHostToDevice, st.s));
-            FEA_CK(cudaMemcpyAsync(dal.p, z, 16, cudaMemcpyHostToDevice, st.s));
+            FEA_CK(cudaMemcpyAsync(ptr_d, z, 8, cudaMemcpyHostToDevice, st.s));
+            FEA_CK(cudaMemcpyAsync(al_d, z, 16, cudaMemcpyHostToDevice, st.s));
         }
-        copy_out(row_ptr, dptr.p, (rows + 1) * 8, st.s);
-        copy_out(col_align, dal.p, (2 * p->n_runs + 2) * 8, st.s);
+        if (dptr.p) copy_out(row_ptr, dptr.p, (rows + 1) * 8, st.s);
+        if (col_align && dal.p) copy_out(col_align, dal.p, (2 * p->n_runs + 2) * 8, st.s);
         FEA_CK(cudaStreamSynchronize(st.s));
     });
 }

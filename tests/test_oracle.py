@@ -302,3 +302,25 @@ def test_degenerate_elements_match_live_reference(orc, ref_lib):
             R.assemble(K, "colour-vec", "csr", threads=2, colour_of=col).tobytes()
         ones = P.assemble_sequential(ed, np.ones_like(K))
         assert ones.sum() == conn.shape[0] * ed.shape[1] ** 2
+
+
+# ---- restricted oracle (config 5 scale: whole row pointers + selected rows) ----
+
+@pytest.mark.parametrize("name", list(CASES) + ["refdofmap_n4_p3_d2"])
+def test_restricted_oracle_matches_reference_fixtures(orc, name):
+    """orc.Adjacency (the full-size check of config 5, NNZ 4.09e9) against arrays made by the
+    unmodified reference: whole CSR / CRAC row pointers, and every node's rows (columns,
+    sequential and colour-vec values with the seeded supplier) bit for bit."""
+    g, conn, nn, d = gold_case(name)
+    A = orc.Adjacency(conn, nn)
+    rp, cp = A.row_ptrs(d, threads=3)
+    assert np.array_equal(rp, g["row_ptr"]) and np.array_equal(cp, g["crac_ptr"])
+    nodes = np.arange(nn)
+    for colour, want in ((None, g["values_seq"]), (g["colour_of"], g["values_colour"])):
+        cnt, cols, vals = A.node_rows(nodes, d, 42, colour_of=colour)
+        for v in nodes:
+            dofs = np.array([u * d + q for u in cols[v, :cnt[v]] for q in range(d)])
+            for k in range(d):
+                a, b = rp[v * d + k], rp[v * d + k + 1]
+                assert np.array_equal(g["cols"][a:b], dofs)
+                assert vals[v, k, :b - a].tobytes() == want[a:b].tobytes()
