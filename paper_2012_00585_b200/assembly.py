@@ -60,10 +60,10 @@ def _ptr(x) -> c_void_p:
     return c_void_p(x.data_ptr())
 
 
-def _stream_ptr(stream) -> c_void_p:
+def _stream_ptr(stream, device: int | None = None) -> c_void_p:
     if stream is None:
         import torch
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(device)
     return c_void_p(stream.cuda_stream)
 
 
@@ -91,10 +91,13 @@ class Plan:
         self._lib = N.lib()
         self.device = device
         self._h = c_void_p(0)
+        self.m = None
+        self._krows = None
         if _handle is not None:
             self._h = _handle
         else:
             dofs, E, m = _as_int64_dofs(elem_dofs)
+            self.m, self._krows = m, (None if k_compact else E)
             rb, re = (0, n_rows) if row_range is None else row_range
             flags = N.FEA_PLAN_K_COMPACT if k_compact else 0
             h = c_void_p(0)
@@ -114,7 +117,9 @@ class Plan:
         h = c_void_p(0)
         _check(lib.fea_plan_create_with_pattern(device, _ptr(dofs), E, m, n_rows, f, _ptr(rp),
                                                 _ptr(ix), byref(h)))
-        return cls(None, n_rows, device=device, _handle=h)
+        plan = cls(None, n_rows, device=device, _handle=h)
+        plan.m, plan._krows = m, E
+        return plan
 
     def _refresh(self):
         r, z, u, e = c_int64(), c_int64(), c_int64(), c_int64()
@@ -123,6 +128,32 @@ class Plan:
         d, npe, meta = c_int32(), c_int32(), c_int64()
         _check(self._lib.fea_plan_info(self._h, byref(d), byref(npe), byref(meta)))
         self.dofs_per_node, self.nodes_per_element, self.metadata_bytes = d.value, npe.value, meta.value
+        if self._krows is None:  # K holds the kept elements only (FEA_PLAN_K_COMPACT)
+            self._krows = self.n_elements
+
+    # argument checks before raw pointers cross the ABI (a short or mistyped buffer would be
+    # read / written out of bounds by the kernels)
+    def _check_k(self, K, host: bool = False):
+        shape = (self._krows, self.m, self.m)
+        if host:
+            assert isinstance(K, np.ndarray) and K.dtype == np.float64 and K.flags["C_CONTIGUOUS"], \
+                "K must be a C-contiguous float64 numpy array"
+            assert K.size == self._krows * self.m * self.m, f"K must hold {shape} doubles"
+            return
+        import torch
+        assert K.dtype == torch.float64 and K.is_cuda and K.is_contiguous(), "K must be contiguous cuda float64"
+        assert K.device.index == self.device, f"K must be on cuda:{self.device}"
+        assert K.numel() == self._krows * self.m * self.m, f"K must hold {shape} doubles"
+
+    def _check_values(self, values, host: bool = False):
+        if host:
+            assert isinstance(values, np.ndarray) and values.dtype == np.float64 and values.flags["C_CONTIGUOUS"]
+            assert values.size >= self.nnz, f"values must hold >= {self.nnz} doubles"
+            return
+        import torch
+        assert values.dtype == torch.float64 and values.is_cuda and values.is_contiguous()
+        assert values.device.index == self.device, f"values must be on cuda:{self.device}"
+        assert values.numel() >= self.nnz, f"values must hold >= {self.nnz} doubles"
 
     # -- symbolic outputs -------------------------------------------------
     def csr(self):
@@ -200,9 +231,11 @@ class Plan:
         if values is None:
             values = torch.zeros(self.nnz, dtype=torch.float64, device=f"cuda:{self.device}")
             accumulate = False
+        self._check_k(K)
+        self._check_values(values)
         flags = (N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE) | _EXTRA_FLAGS.get(strategy, 0)
         _check(self._lib.fea_assemble(self._h, _ptr(K), STRATEGIES[strategy], _ptr(values), flags,
-                                      _stream_ptr(stream)))
+                                      _stream_ptr(stream, self.device)))
         return values
 
     def assemble_into(self, K, values_ptr: int, strategy: str = "sorted", accumulate: bool = False,
@@ -210,9 +243,10 @@ class Plan:
         """Assemble into a raw device address (e.g. this rank's row block inside the root's
         global values buffer, mapped with dist.PeerValues): the kernel's stores go to wherever
         the pointer lives, peer memory over NVLink included."""
+        self._check_k(K)
         flags = (N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE) | _EXTRA_FLAGS.get(strategy, 0)
         _check(self._lib.fea_assemble(self._h, _ptr(K), STRATEGIES[strategy], c_void_p(values_ptr), flags,
-                                      _stream_ptr(stream)))
+                                      _stream_ptr(stream, self.device)))
 
     def assemble_seeded(self, seed: int, values=None, strategy: str = "sorted", accumulate: bool = False,
                         stream=None):
@@ -221,9 +255,10 @@ class Plan:
         if values is None:
             values = torch.zeros(self.nnz, dtype=torch.float64, device=f"cuda:{self.device}")
             accumulate = False
+        self._check_values(values)
         flags = (N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE) | _EXTRA_FLAGS.get(strategy, 0)
         _check(self._lib.fea_assemble_seeded(self._h, ctypes.c_uint64(seed), STRATEGIES[strategy],
-                                             _ptr(values), flags, _stream_ptr(stream)))
+                                             _ptr(values), flags, _stream_ptr(stream, self.device)))
         return values
 
     def assemble_host(self, K_host, values_host=None, strategy: str = "sorted",
@@ -232,9 +267,11 @@ class Plan:
         if values_host is None:
             values_host = np.zeros(self.nnz, np.float64)
             accumulate = False
+        self._check_k(K_host, host=True)
+        self._check_values(values_host, host=True)
         flags = (N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE) | _EXTRA_FLAGS.get(strategy, 0)
         _check(self._lib.fea_assemble_host(self._h, _ptr(K_host), STRATEGIES[strategy],
-                                           _ptr(values_host), flags, _stream_ptr(stream)))
+                                           _ptr(values_host), flags, _stream_ptr(stream, self.device)))
         return values_host
 
     def set_host_windows(self, n_windows: int) -> None:
@@ -247,11 +284,14 @@ class Plan:
         Step i's K upload overlaps step i-1's kernel and values download (pinned memory)."""
         n = len(K_hosts)
         assert len(values_hosts) == n
+        for k, v in zip(K_hosts, values_hosts):
+            self._check_k(k, host=True)
+            self._check_values(v, host=True)
         kp = (c_void_p * max(n, 1))(*[_ptr(k).value for k in K_hosts])
         vp = (c_void_p * max(n, 1))(*[_ptr(v).value for v in values_hosts])
         flags = (N.FEA_ACCUMULATE if accumulate else N.FEA_OVERWRITE) | _EXTRA_FLAGS.get(strategy, 0)
         _check(self._lib.fea_assemble_host_batch(self._h, kp, STRATEGIES[strategy], vp, n, flags,
-                                                 _stream_ptr(stream)))
+                                                 _stream_ptr(stream, self.device)))
         return values_hosts
 
     def spmv(self, values, x, y=None, stream=None):
@@ -259,7 +299,7 @@ class Plan:
         import torch
         if y is None:
             y = torch.empty(self.n_rows, dtype=torch.float64, device=values.device)
-        _check(self._lib.fea_plan_spmv(self._h, _ptr(values), _ptr(x), _ptr(y), _stream_ptr(stream)))
+        _check(self._lib.fea_plan_spmv(self._h, _ptr(values), _ptr(x), _ptr(y), _stream_ptr(stream, self.device)))
         return y
 
     def close(self) -> None:
@@ -289,7 +329,7 @@ def fill_seeded_k(n: int, m: int, seed: int, elem_ids=None, device: int = 0, out
     if elem_ids is not None:
         ids = torch.as_tensor(elem_ids, dtype=torch.int64, device=out.device).contiguous()
     _check(N.lib().fea_fill_seeded_k(_ptr(out), n, m, ctypes.c_uint64(seed), _ptr(ids),
-                                     _stream_ptr(stream)))
+                                     _stream_ptr(stream, out.device.index)))
     if ids is not None:
         torch.cuda.current_stream(out.device).synchronize()
     return out
@@ -302,7 +342,7 @@ def spmv_csr(row_ptr, cols, values, x, y=None, stream=None):
     if y is None:
         y = torch.empty(n, dtype=torch.float64, device=values.device)
     _check(N.lib().fea_spmv_csr(_ptr(row_ptr), _ptr(cols), _ptr(values), n, _ptr(x), _ptr(y),
-                                _stream_ptr(stream)))
+                                _stream_ptr(stream, values.device.index)))
     return y
 
 
@@ -313,5 +353,5 @@ def spmv_crac(crac_ptr, col_align, values, x, y=None, stream=None):
     if y is None:
         y = torch.empty(n, dtype=torch.float64, device=values.device)
     _check(N.lib().fea_spmv_crac(_ptr(crac_ptr), _ptr(col_align), _ptr(values), n, _ptr(x), _ptr(y),
-                                 _stream_ptr(stream)))
+                                 _stream_ptr(stream, values.device.index)))
     return y

@@ -176,13 +176,17 @@ public:
         return pos ? values.v[*pos] : 0.0;
     }
 
-    // plan for this element set (cached)
+    // plan for this element set, cached by CONTENT: the reference keeps no element state and
+    // locates every entry on every assembly, so a job whose DOFs changed (edited in place, or
+    // a reused buffer) must not run on the old slot map. Flattening is O(E*m), against the
+    // O(E*m^2) supplier loop of every assembly.
     fea_plan* plan_for(std::span<const ElementDofs> els) {
-        if (plan_ && els.data() == plan_elems_ && els.size() == plan_n_) return plan_;
+        int32_t m = 1;
+        std::vector<index_t> flat = detail::flatten(els, m);
+        if (plan_ && m == m_ && flat == plan_flat_) return plan_;
         if (plan_) fea_plan_destroy(plan_);
         plan_ = nullptr;
-        int32_t m = 1;
-        const std::vector<index_t> flat = detail::flatten(els, m);
+        plan_flat_.clear();
         fea_plan* p = nullptr;
         const bool crac = format_ == FEA_FORMAT_CRAC;
         detail::check(fea_plan_create_with_pattern(
@@ -190,8 +194,7 @@ public:
             crac ? crac_ptr_.data() : pattern_.row_ptr.data(),
             crac ? col_align_.data() : pattern_.cols.data(), &p));
         plan_ = p;
-        plan_elems_ = els.data();
-        plan_n_ = els.size();
+        plan_flat_ = std::move(flat);
         m_ = m;
         return plan_;
     }
@@ -241,8 +244,7 @@ protected:
     int device_;
     std::vector<index_t> crac_ptr_, col_align_;
     fea_plan* plan_ = nullptr;
-    const ElementDofs* plan_elems_ = nullptr;
-    size_t plan_n_ = 0;
+    std::vector<index_t> plan_flat_;  // the DOFs the cached plan was built for
     int32_t m_ = 1;
 };
 

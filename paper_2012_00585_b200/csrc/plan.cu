@@ -1191,6 +1191,10 @@ fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, in
         std::vector<int64_t> h_ptr(static_cast<size_t>(n_rows + 1));
         FEA_CK(cudaMemcpy(h_ptr.data(), row_ptr, h_ptr.size() * 8, cudaMemcpyDefault));
         std::vector<int64_t> h_csr_ptr, h_cols, h_crac_ptr, h_align;
+        FEA_REQUIRE(h_ptr[0] == 0, FEA_ERR_INVALID, "row_ptr[0] must be 0");
+        for (int64_t r = 0; r < n_rows; ++r)
+            FEA_REQUIRE(h_ptr[r] <= h_ptr[r + 1], FEA_ERR_INVALID, "row_ptr not monotone");
+        FEA_REQUIRE(h_ptr[n_rows] <= (int64_t{1} << 40), FEA_ERR_INVALID, "row_ptr[n_rows] out of range");
         if (format == FEA_FORMAT_CSR) {
             h_csr_ptr = h_ptr;
             h_cols.resize(static_cast<size_t>(h_ptr[n_rows]));
@@ -1198,9 +1202,23 @@ fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, in
                 FEA_CK(cudaMemcpy(h_cols.data(), idx, h_cols.size() * 8, cudaMemcpyDefault));
         } else {
             h_crac_ptr = h_ptr;
+            // build_crac_arrays layout (formats.cpp:21-41): row_ptr in col_align entry units, even,
+            // 2 * runs at the end; pairs (column start, values position) with the final (0, nnz)
+            for (int64_t r = 0; r <= n_rows; ++r)
+                FEA_REQUIRE((h_ptr[r] & 1) == 0, FEA_ERR_INVALID, "CRAC row_ptr entries must be even");
             const int64_t n_align = h_ptr[n_rows] + 2;
             h_align.resize(static_cast<size_t>(n_align));
             FEA_CK(cudaMemcpy(h_align.data(), idx, h_align.size() * 8, cudaMemcpyDefault));
+            // every run's values position is the running count of the runs before it, and run
+            // lengths (next position - this one) are positive: the CSR view below then has
+            // exactly h_align[last + 1] entries in values order
+            for (int64_t i = 0; i + 2 < n_align; i += 2) {
+                FEA_REQUIRE(h_align[i] >= 0 && h_align[i + 3] > h_align[i + 1] && h_align[1] == 0,
+                            FEA_ERR_INVALID, "CRAC runs: value positions must start at 0 and increase");
+                FEA_REQUIRE(h_align[i] + (h_align[i + 3] - h_align[i + 1]) <= n_rows, FEA_ERR_INVALID,
+                            "CRAC run extends past the last column");
+            }
+            FEA_REQUIRE(n_align > 2 || h_align[1] == 0, FEA_ERR_INVALID, "CRAC pattern without runs must have nnz 0");
             // CSR view of the CRAC pattern (for_each_in_row, formats.hpp:315-324)
             h_csr_ptr.resize(static_cast<size_t>(n_rows + 1));
             for (int64_t r = 0; r < n_rows; ++r) {

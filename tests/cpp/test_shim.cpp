@@ -132,6 +132,29 @@ int main() {
         }
         CHECK(named);
     }
+    // The target keeps no element state between assemblies (the reference locates every entry
+    // on every call): the same element vector edited in place must be located afresh — a DOF
+    // moved outside the pattern is an AssemblyError, a DOF moved inside it lands in its new slot.
+    {
+        index_t nd;
+        auto dofs = structured_dofs(2, 1, &nd);
+        const SparsityPattern partial = build_pattern(std::span<const ElementDofs>(dofs).first(1), nd);
+        CsrMatrix m(partial);
+        std::vector<ElementDofs> first(dofs.begin(), dofs.begin() + 1);
+        assemble_sequential(m, AssemblyJob{first, ones_supplier(4), 1});
+        CHECK(values_total(m) == 16.0);
+        first[0].flat = dofs[1].flat;  // same buffer, same size, different element
+        first[0].runs = encode_runs(first[0].flat);
+        CHECK_THROWS_AS(assemble_sequential(m, AssemblyJob{first, ones_supplier(4), 1}), AssemblyError);
+        CsrMatrix full(build_pattern(dofs, nd));
+        std::vector<ElementDofs> one(dofs.begin(), dofs.begin() + 1);
+        assemble_sequential(full, AssemblyJob{one, ones_supplier(4), 1});
+        one[0].flat = dofs[3].flat;
+        one[0].runs = encode_runs(one[0].flat);
+        assemble_sequential(full, AssemblyJob{one, ones_supplier(4), 1});
+        // the centre node (4) is shared by both elements: 2 contributions on its diagonal
+        CHECK(full.get(4, 4) == 2.0 && full.get(0, 0) == 1.0 && full.get(8, 8) == 1.0);
+    }
     // test_assembly.cpp:143-184 / acceptance.cpp:180-199 — all methods bitwise equal with ones
     {
         index_t nd;

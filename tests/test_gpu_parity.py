@@ -17,6 +17,9 @@ TOL = 1e-12  # reference tolerance form, test_assembly.cpp:236 / acceptance.cpp:
 
 CASES = [
     ("quad4", 6, 1, None),
+    ("quad4", 4, 5, None),          # d >= 5: the generic gathers and k_scatter atomics
+    ("quad4", 3, 8, "nodes"),       # the paper's d-benchmark goes up to 8
+    ("hex8", 2, 5, "elements"),
     ("quad4", 5, 4, "nodes"),
     ("hex8", 3, 3, "elements"),
     ("hex8", 4, 2, None),
@@ -165,6 +168,29 @@ def test_external_pattern_superset(gpu, orc, fmt):
         assert got.tobytes() == want.tobytes()
         got_a = plan.assemble(torch.from_numpy(Kh).cuda(), strategy="atomic").cpu().numpy()
         assert close(got_a, want)
+
+
+def test_external_pattern_malformed_is_invalid(gpu, orc):
+    """Malformed caller patterns are refused with FEA_ERR_INVALID (ValueError) before any
+    indexing: row_ptr[0] != 0, decreasing row_ptr, odd CRAC row pointers, CRAC value positions
+    that do not follow the runs, columns outside the matrix."""
+    conn, nn, ed, n_rows = problem("quad4", 3, 1, None)
+    P = orc.Pattern.build(conn, nn, 1)
+    rp, cs = P.arrays()
+    cp, ca = P.crac()
+    bad = []
+    r = rp.copy(); r[0] = 1; bad.append((r, cs, "csr"))
+    r = rp.copy(); r[3] = r[4] + 1; bad.append((r, cs, "csr"))
+    c = cs.copy(); c[5] = n_rows + 7; bad.append((rp, c, "csr"))
+    r = cp.copy(); r[2] += 1; bad.append((r, ca, "crac"))
+    a = ca.copy(); a[3] = a[5] + 2; bad.append((cp, a, "crac"))
+    a = ca.copy(); a[-1] = a[-3]; bad.append((cp, a, "crac"))
+    a = ca.copy(); a[-4] = n_rows; bad.append((cp, a, "crac"))
+    for r, c, fmt in bad:
+        with pytest.raises(ValueError):
+            gpu.Plan.with_pattern(ed, n_rows, r, c, fmt)
+    with gpu.Plan.with_pattern(ed, n_rows, cp, ca, "crac") as plan:  # the well-formed one
+        assert plan.nnz == P.nnz
 
 
 def test_missing_entry_is_assembly_error(gpu, orc):
@@ -606,3 +632,23 @@ def test_cuda_graph_replay(gpu, orc, mesh, n, d, perm):
                 assert close(got, want)
             elif strategy == "sorted":
                 assert got.tobytes() == want.tobytes()
+
+
+def test_binding_rejects_bad_buffers(gpu):
+    """Plan.assemble* check dtype, size and device of K / values before raw pointers cross the
+    ABI (a float32 or short K would be read out of bounds by the kernels)."""
+    import torch
+    conn, nn, ed, n_rows = problem("hex8", 2, 3, None)
+    E, m = ed.shape
+    with gpu.Plan(ed, n_rows, dofs_per_node=3) as plan:
+        good = gpu.fill_seeded_k(E, m, 1)
+        v = plan.assemble(good)
+        for K in (good.float(), good[:-1], good.cpu()):
+            with pytest.raises(AssertionError):
+                plan.assemble(K)
+        with pytest.raises(AssertionError):
+            plan.assemble(good, v[:-1])
+        with pytest.raises(AssertionError):
+            plan.assemble_host(good.cpu().numpy().astype(np.float32))
+        with pytest.raises(AssertionError):
+            plan.assemble_seeded(1, v[:-1])
