@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import sys
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -162,9 +163,13 @@ def cmd_assemble(a) -> int:
     print(f"mesh {label}: {plan.n_rows} dofs, {plan.nnz} nnz, {plan.n_runs} runs; method {a.method}, "
           f"format {a.format}: {t:.2f} us")
     if a.dump:
+        # fea_main.cpp:239-253: the dump is ones_supplier + assemble_sequential into CSR
+        ones = torch.ones_like(K)
+        dumped = plan.assemble(ones, strategy="sorted")
         rp, cs = plan.csr()
         with open(a.dump, "w") as f:
-            write_matrix_market(rp, cs, values.cpu().numpy(), f)
+            write_matrix_market(rp, cs, dumped.cpu().numpy(), f)
+        print(f"wrote {a.dump}")
     return EXIT_OK
 
 
@@ -201,40 +206,92 @@ def cmd_bench(a) -> int:
     return EXIT_OK
 
 
-def cmd_verify(a) -> int:
+@dataclass
+class VerifyResult:
+    """fea::VerifyResult (verify.hpp:38-45)."""
+    ok: bool = True
+    dofs: int = 0
+    nnz: int = 0
+    expected_total: float = 0.0
+    checked: list = field(default_factory=list)
+    failures: list = field(default_factory=list)
+
+
+def _compare_values(combo, got, want, expected_total, out: VerifyResult) -> None:
+    """compare_values (verify.cpp:31-54): first differing slot by bit pattern, then the exact
+    total; messages in the reference's wording (std::to_string -> %f)."""
+    if got.size != want.size:
+        out.failures.append(f"{combo}: values length mismatch")
+        return
+    diff = np.flatnonzero(got.view(np.int64) != want.view(np.int64))
+    if diff.size:
+        i = int(diff[0])
+        out.failures.append(f"{combo}: values[{i}] = {got[i]:f}, sequential has {want[i]:f}")
+        return
+    total = float(np.sum(got))
+    if total != expected_total:
+        out.failures.append(f"{combo}: total {total:f} != expected {expected_total:f}")
+
+
+def verify_methods(conn, n_nodes: int, d: int, tamper=None) -> VerifyResult:
     """verify_methods (verify.cpp:70-156) on the GPU: ones element matrices, every GPU method on
-    both formats, bitwise equal to seq/csr, total exactly E*m^2."""
+    both formats, bitwise equal to seq/csr and totals exactly E*m^2. `tamper(combo, values)`
+    is the reference's test hook (VerifyOptions::tamper, verify.hpp:31-36), called with each
+    combination's host values right after its assembly. The spin methods have no GPU
+    counterpart, so 6 combinations are checked (the reference checks 10)."""
     import torch
-    label, n, conn, nn = parse_mesh(a.mesh)
-    plan = _plan(conn, nn, a.d)
+    plan = _plan(conn, n_nodes, d)
     plan.set_colouring(plan.greedy_colouring()[0])
-    E, m = conn.shape[0], conn.shape[1] * a.d
-    K = torch.ones((E, m, m), dtype=torch.float64, device="cuda")
-    expected = float(E) * m * m
-    failures, checked = [], []
-    ref = plan.assemble(K, strategy="sorted").clone()
-    if float(ref.sum().item()) != expected:
-        failures.append(f"seq/csr: total {float(ref.sum().item())} != expected {expected}")
-    checked.append("seq/csr")
-    for fmt in FORMATS:
-        for meth in METHODS:
+    E, m = conn.shape[0], conn.shape[1] * d
+    K = torch.ones((E, m, m), dtype=torch.float64, device=f"cuda:{plan.device}")
+    out = VerifyResult(dofs=plan.n_rows, nnz=plan.nnz, expected_total=float(E) * m * m)
+    ref = plan.assemble(K, strategy="sorted").cpu().numpy()
+    total = float(np.sum(ref))
+    if total != out.expected_total:
+        out.failures.append(f"seq/csr: total {total:f} != expected {out.expected_total:f}")
+    out.checked.append("seq/csr")
+    for meth in METHODS:
+        for fmt in FORMATS:
             combo = f"{meth}/{fmt}"
             if combo == "seq/csr":
                 continue
-            got = plan.assemble(K, strategy=METHODS[meth])
-            diff = torch.nonzero(got != ref)
-            if diff.numel():
-                i = int(diff[0])
-                failures.append(f"{combo}: values[{i}] = {float(got[i])}, sequential has {float(ref[i])}")
-            elif float(got.sum().item()) != expected:
-                failures.append(f"{combo}: total {float(got.sum().item())} != expected {expected}")
-            checked.append(combo)
-    print(f"mesh {label}: {plan.n_rows} dofs, {plan.nnz} nnz, expected total {expected:.0f}")
-    for c in checked:
-        print(f"  {c:16s} {'FAIL' if any(f.startswith(c + ':') for f in failures) else 'ok'}")
-    for f in failures:
-        print("error:", f)
-    return EXIT_OK if not failures else EXIT_VERIFY_FAILED
+            got = plan.assemble(K, strategy=METHODS[meth]).cpu().numpy()
+            if tamper is not None:
+                tamper(combo, got)
+            _compare_values(combo, got, ref, out.expected_total, out)
+            out.checked.append(combo)
+    out.ok = not out.failures
+    return out
+
+
+def parse_tamper(spec):
+    """--tamper COMBO:INDEX[:DELTA] -> a tamper hook adding DELTA (default 1.0) to values[INDEX]
+    of that combination (the reference's test hook exposed on the command line)."""
+    if not spec:
+        return None
+    parts = spec.split(":")
+    if len(parts) not in (2, 3) or parts[0] not in [f"{m}/{f}" for m in METHODS for f in FORMATS]:
+        raise UsageError(f"--tamper '{spec}': expected METHOD/FORMAT:INDEX[:DELTA]")
+    combo, idx = parts[0], int(parts[1])
+    delta = float(parts[2]) if len(parts) == 3 else 1.0
+
+    def hook(c, values):
+        if c == combo:
+            values[idx] += delta
+    return hook
+
+
+def cmd_verify(a) -> int:
+    """fea verify (fea_main.cpp:305-318): exit 0 when every combination matches, 2 otherwise."""
+    label, n, conn, nn = parse_mesh(a.mesh)
+    res = verify_methods(conn, nn, a.d, tamper=parse_tamper(a.tamper))
+    print(f"dofs: {res.dofs}, nnz: {res.nnz}, combinations: {len(res.checked)}, threads: {a.threads}")
+    if res.ok:
+        print("verify: OK (all methods bitwise identical, totals exact)")
+        return EXIT_OK
+    for f in res.failures:
+        print(f"verify: FAIL {f}")
+    return EXIT_VERIFY_FAILED
 
 
 def cmd_colour(a) -> int:
@@ -281,6 +338,8 @@ def build_parser() -> argparse.ArgumentParser:
     s.add_argument("--p", type=int, default=1)
     s.add_argument("--d", type=int, default=1)
     s.add_argument("--threads", type=int, default=1)
+    s.add_argument("--tamper", default=None,
+                   help="test hook: METHOD/FORMAT:INDEX[:DELTA] corrupts one slot of that combination")
     s = sub.add_parser("colour", help="Greedy element colouring report")
     s.add_argument("--mesh", default="gen:8")
     s.add_argument("--p", type=int, default=1)

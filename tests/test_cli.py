@@ -53,6 +53,19 @@ def test_matrix_market_dump():
     assert lines[2] == "1 1 1.21" and lines[9] == "3 6 3.3300000000000001"
 
 
+def test_tamper_spec_parsing():
+    hook = cli.parse_tamper("atomic/crac:3")
+    v = np.zeros(5)
+    hook("atomic/csr", v)
+    assert v.sum() == 0
+    hook("atomic/crac", v)
+    assert v[3] == 1.0
+    for bad in ("spin/crac:3", "atomic:3", "atomic/crac"):
+        with pytest.raises(cli.UsageError):
+            cli.parse_tamper(bad)
+    assert cli.main(["verify", "--tamper", "bogus"]) == cli.EXIT_USAGE
+
+
 @pytest.mark.gpu
 def test_verify_bench_assemble_on_gpu(gpu, tmp_path):
     assert cli.main(["verify", "--mesh", "hex8:4:perm-elements", "--d", "3"]) == cli.EXIT_OK
@@ -65,3 +78,53 @@ def test_verify_bench_assemble_on_gpu(gpu, tmp_path):
     mm = (tmp_path / "a.mtx").read_text().splitlines()
     assert mm[1] == "9 9 49"  # (3n+1)^2, n = 2
     assert cli.main(["colour", "--mesh", "gen:6", "--out", str(tmp_path / "c.csv")]) == cli.EXIT_OK
+
+
+@pytest.mark.gpu
+def test_verify_reports_tampered_slot(gpu, capsys):
+    """test_assembly.cpp:350-374: a clean run is ok; a corrupted slot of one combination makes
+    verify fail (exit 2) and the first failure names that combination and the slot."""
+    res = cli.verify_methods(*cli.parse_mesh("gen:4")[2:], d=2)
+    assert res.ok and not res.failures and len(res.checked) == 6  # the reference: 10 (4 spin combos)
+
+    def tamper(combo, values):
+        if combo == "atomic/crac":
+            values[3] += 1.0
+    res = cli.verify_methods(*cli.parse_mesh("gen:4")[2:], d=1, tamper=tamper)
+    assert not res.ok and len(res.failures) >= 1
+    assert "atomic/crac" in res.failures[0] and "values[3]" in res.failures[0]
+    capsys.readouterr()
+    assert cli.main(["verify", "--mesh", "gen:4", "--tamper", "colour-vec/csr:7:0.5"]) == cli.EXIT_VERIFY_FAILED
+    outp = capsys.readouterr().out
+    assert "verify: FAIL colour-vec/csr: values[7]" in outp and "combinations: 6" in outp
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mesh,d", [("gen:5", 2), ("hex8:3:perm-elements", 3), ("tet4:3:perm-nodes", 1)])
+def test_dump_and_bench_csv_match_oracle(gpu, orc, tmp_path, mesh, d):
+    """`assemble --dump` (fea_main.cpp:239-253: ones supplier, assemble_sequential, Matrix Market
+    formats.hpp:366-379) is byte-identical to the oracle's matrix through the same writer; the
+    bench CSV's dofs / nnz / storage factor equal the oracle's pattern (bench.cpp:100-113)."""
+    import io
+    _, _, conn, nn = cli.parse_mesh(mesh)
+    from paper_2012_00585_b200 import meshgen as M
+    ed = M.element_dofs(conn, d)
+    P = orc.Pattern.build(conn, nn, d)
+    want = P.assemble_sequential(ed, np.ones((ed.shape[0], ed.shape[1], ed.shape[1])))
+    rp, cs = P.arrays()
+    buf = io.StringIO()
+    cli.write_matrix_market(rp, cs, want, buf)
+    path = tmp_path / "a.mtx"
+    assert cli.main(["assemble", "--mesh", mesh, "--d", str(d), "--dump", str(path)]) == cli.EXIT_OK
+    assert path.read_text() == buf.getvalue()
+    out = tmp_path / "b"
+    assert cli.main(["bench", "--mesh", mesh, "--d", str(d), "--runs", "2", "--out", str(out)]) == cli.EXIT_OK
+    lines = (tmp_path / "b.summary.csv").read_text().splitlines()
+    hdr = lines[0].split(",")
+    for line in lines[1:]:
+        row = dict(zip(hdr, line.split(",")))
+        assert int(row["dofs"]) == P.n_rows and int(row["nnz"]) == P.nnz
+        assert float(row["gamma"]) == pytest.approx((2 * P.n_runs + 2) / P.nnz, abs=1e-6)
+        assert float(row["values_mb"]) == pytest.approx(8.0 * P.nnz / 1e6, abs=1e-6)
+    raw = (tmp_path / "b.raw.csv").read_text().splitlines()
+    assert len(raw) == 1 + 6 * 2 and all(float(r.split(",")[-1]) > 0 for r in raw[1:])
