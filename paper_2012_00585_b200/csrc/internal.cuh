@@ -59,7 +59,7 @@ struct DeviceScope {
 // Environment A/B switches of the numeric kernels, read once per process
 // instead of on every assembly.
 struct Knobs {
-    bool atomic_legacy, slot_no_fixed, cn_unpacked, cn_no_records, d1_no_direct, d1_no_vec;
+    bool atomic_legacy, atomic_no_patch, slot_no_fixed, cn_unpacked, cn_no_records, d1_no_direct, d1_no_vec;
     int d1_acc_mod, d1v_acc_mod;  // accumulator stride residues (mod 16 doubles)
 };
 const Knobs& knobs();
@@ -127,6 +127,17 @@ struct fea_plan {
     feagpu::DevBuf at_rows;   // int64 [at_E_pad*npe] values start << 20 | row length (-1: not owned)
     feagpu::DevBuf at_pos;    // PosT [at_E_pad*npe*npe] row-relative positions
     int64_t at_E_pad = 0;     // E rounded up to whole warp steps
+    // atomic route with patch pre-reduction (k_atomic_patch; npe = 8, lazy): patches of <= 8
+    // node-sharing elements, their distinct (row node, column node) pairs and per element the
+    // pair index of every (a, b)
+    feagpu::DevBuf pk_hdr;    // int4 [pk_n]: -, pair offset, row offset, n_elems | n_rows << 8 | n_pairs << 16
+    feagpu::DevBuf pk_krow;   // int32 [pk_n*8] K row per element slot (-1: empty slot)
+    feagpu::DevBuf pk_cidx;   // uint16 [pk_n*8*64] pair index per (slot, a, b) (0xffff: row not owned)
+    feagpu::DevBuf pk_rows;   // int64 [] values start << 20 | row length per patch row node
+    feagpu::DevBuf pk_rowpair;  // int32 [] first pair of the row | pair count << 16 (pairs sorted by row)
+    feagpu::DevBuf pk_pairs;  // uint16 [] row index << 8 | position per distinct pair
+    int64_t pk_n = 0;
+    int32_t pk_max_pairs = 0;
     feagpu::DevBuf node_order;  // int32 [n_own] gather traversal order (empty: node id order)
     // d = 1 with a traversal order: the sorted incidences re-laid in traversal order, so the
     // gather reads them sequentially (else: random 128 B line fetches per node)

@@ -4,6 +4,7 @@
 #pragma once
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -115,6 +116,11 @@ __device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint3
         "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
         "l"(src), "r"(bytes), "r"(bar), "l"(policy)
         : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
@@ -1609,6 +1615,199 @@ __global__ void k_atomic_maps(const int32_t* __restrict__ order, const int32_t* 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Atomic route with patch pre-reduction (hex8-type shapes: npe = 8, d <= 3)
+// ---------------------------------------------------------------------------
+// k_atomic_staged issues one RED per element-matrix entry: cfg2's 151 M lanes become 64.6 M
+// L2 reduction sectors, and that sector rate (~115e9/s), not HBM, bounds the route. Elements
+// that share nodes add into the same d x d node-pair blocks, so the plan groups the elements
+// into patches of up to P = 8 node-sharing elements (greedy growth by shared nodes from the
+// visit order: 2 x 2 x 2 blocks on structured meshes, 343 distinct node pairs for 512 element
+// node pairs) and lists each patch's distinct (row node, column node) pairs sorted by (row,
+// position). A CTA owns a patch: it streams the patch's element blocks through shared memory
+// (cp.async, STAGES - 1 elements ahead), adds every entry into the patch accumulator
+// acc[pair][ki][kj] in shared memory (one element at a time, CTA barrier between elements:
+// within an element the (a, b) node pairs are distinct, so threads never collide), then
+// flushes it row by row — a warp per patch row, lanes over (ki, pair, kj), so the REDs of one
+// warp instruction cover the row's consecutive pairs at consecutive addresses — with one RED
+// per distinct slot. Conflicts between patches are still resolved by atomics only: this IS
+// the atomic route (assemble_atomic, assembly.hpp:121-126), with fewer and denser reductions.
+// Values match assemble_sequential within the reference tolerance (the pre-reduction changes
+// the summation order like any atomic schedule does).
+#ifndef FEA_PATCH_K_HINT
+// K copies with an L2 evict-first policy: ptxas 12.9 folded the createpolicy of the first form
+// of this kernel into uniform registers and then encoded the copies with unset descriptor
+// registers (the launch died with "illegal instruction"); plain cp.async by default
+#define FEA_PATCH_K_HINT 0
+#endif
+#ifndef FEA_PATCH_WARPS
+#define FEA_PATCH_WARPS 4
+#endif
+constexpr int kPatchElems = 8;  // elements per patch (a 2 x 2 x 2 block of hex8)
+constexpr int kPatchWarps = FEA_PATCH_WARPS;
+template <int D, int NPE, int P, int STAGES>
+__global__ void __launch_bounds__(kPatchWarps * 32)
+    k_atomic_patch(const double* __restrict__ K, const int4* __restrict__ hdr, const int32_t* __restrict__ pk_krow,
+                   const uint16_t* __restrict__ pk_cidx, const int64_t* __restrict__ pk_rows,
+                   const int32_t* __restrict__ pk_rowpair, const uint16_t* __restrict__ pk_pairs, int64_t n_patch,
+                   int acc_doubles, double* __restrict__ values) {
+    constexpr int M = D * NPE, MM = M * M, DD = D * D, NN = NPE * NPE;
+    constexpr int KB = MM * 8, CB = NN * 2, SLOT = KB + CB;
+    constexpr int NT = kPatchWarps * 32;
+    constexpr int T = (MM + NT - 1) / NT;  // entries per thread per element
+    static_assert(KB % 16 == 0 && CB % 16 == 0, "16-byte bulk copies");
+    extern __shared__ __align__(16) unsigned char smem_pa[];
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    double* acc = reinterpret_cast<double*>(smem_pa);
+    unsigned char* stg = smem_pa + static_cast<size_t>(acc_doubles) * 8;
+    // the patch's flush tables, staged once per patch (loaded into registers early in the
+    // patch, stored before the flush): rows (values start | length), row pair ranges, pairs
+    constexpr int MAXR = P * NPE, MAXP = P * NN;
+    constexpr int PPT = (MAXP + NT - 1) / NT;
+    int64_t* s_rows = reinterpret_cast<int64_t*>(stg + STAGES * SLOT);
+    int32_t* s_rowpair = reinterpret_cast<int32_t*>(s_rows + MAXR);
+    uint16_t* s_pairs = reinterpret_cast<uint16_t*>(s_rowpair + MAXR);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_pairs + MAXP);  // one mbarrier per stage
+    int64_t m_row = 0;
+    int32_t m_rowpair = 0;
+    uint16_t m_pair[PPT];
+    const int64_t G = gridDim.x;
+    if (static_cast<int64_t>(blockIdx.x) >= n_patch) return;
+    if (tid == 0) {
+        for (int st = 0; st < STAGES; ++st) mbar_init(smem_u32(bars + st), 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    // issue cursor (STAGES - 1 element slots ahead of the fold): patch and slot. Thread 0
+    // copies a slot's K block (4.6 KB contiguous) and its pair indices with two bulk copies.
+    int64_t ipt = blockIdx.x;
+    int ik = 0;
+    auto advance = [&]() {
+        if (++ik == P) {
+            ik = 0;
+            ipt += G;
+        }
+    };
+    auto krow_at = [&]() -> int32_t { return ipt < n_patch ? __ldg(pk_krow + ipt * P + ik) : -1; };
+    auto issue = [&](int stage, int32_t kr) {  // the slot at the cursor (thread 0 only)
+        const uint32_t bar = smem_u32(bars + stage);
+        if (kr >= 0) {
+            unsigned char* sb = stg + stage * SLOT;
+            fence_proxy_async_smem();  // the stage was last read by generic loads
+            mbar_arrive_expect_tx(bar, SLOT);
+            bulk_g2s(smem_u32(sb), K + static_cast<int64_t>(kr) * MM, KB, bar);
+            bulk_g2s(smem_u32(sb + KB), pk_cidx + (ipt * P + ik) * NN, CB, bar);
+        } else {
+            mbar_arrive(bar);  // empty slot: complete the phase without data
+        }
+    };
+    // this thread's entries of an element block, decoded once into byte offsets: the entry's
+    // pair-index slot in the staged indices and its (ki, kj) offset inside a pair's block
+    uint32_t cio[T], co8[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        const int idx = min(tid + NT * t, MM - 1);
+        const int i = idx / M, jj = idx - (idx / M) * M;
+        cio[t] = static_cast<uint32_t>(((i / D) * NPE + jj / D) * 2);
+        co8[t] = static_cast<uint32_t>(((i % D) * D + jj % D) * 8);
+        // passed through a shuffle so the code generator keeps them in registers instead of
+        // re-deriving them (two magic-number divisions and a dozen integer ops) for every entry
+        // of every element (an empty asm does not stop ptxas from rematerializing)
+        cio[t] = __shfl_sync(0xffffffffu, cio[t], lane);
+        co8[t] = __shfl_sync(0xffffffffu, co8[t], lane);
+    }
+    constexpr int FQ = 32 / D;  // flush: lane = (pair in a chunk of FQ, kj), ki looped
+    const int fq = lane / D, fkj = lane - (lane / D) * D;
+    int32_t kr_next = -1;
+    if (tid == 0) {
+#pragma unroll
+        for (int k = 0; k < STAGES - 1; ++k) {
+            issue(k, krow_at());
+            advance();
+        }
+        kr_next = krow_at();
+    }
+    int4 h = make_int4(0, 0, 0, 0);
+    int64_t pt = blockIdx.x;
+    int k = 0, stage = 0;
+    uint32_t phase = 0;  // bit st: parity of stage st's next completion
+    for (; pt < n_patch;) {
+        if (k == 0) {  // patch start: header, zero the accumulator (the barrier below orders it)
+            h = __ldg(hdr + pt);
+            const int n_pairs = static_cast<int>(static_cast<uint32_t>(h.w) >> 16);
+            for (int f = tid; f < (n_pairs + 1) * DD; f += NT) acc[f] = 0.0;  // + the spare pair
+        }
+        mbar_wait(smem_u32(bars + stage), (phase >> stage) & 1u);
+        phase ^= 1u << stage;
+        __syncthreads();  // the previous slot's adds are done (acc ordering, stage reuse)
+        if (tid == 0) {
+            issue((stage + STAGES - 1) % STAGES, kr_next);
+            advance();
+            kr_next = krow_at();
+        }
+        if (k == (P > 1 ? 1 : 0)) {  // this patch's flush tables: loads in flight during the adds
+            const int n_rows = (h.w >> 8) & 0xff, n_pairs = static_cast<int>(static_cast<uint32_t>(h.w) >> 16);
+            if (tid < n_rows) {
+                m_row = __ldg(pk_rows + h.z + tid);
+                m_rowpair = __ldg(pk_rowpair + h.z + tid);
+            }
+#pragma unroll
+            for (int u = 0; u < PPT; ++u)
+                m_pair[u] = tid + NT * u < n_pairs ? __ldg(pk_pairs + h.y + tid + NT * u) : uint16_t(0);
+        }
+        if (k < (h.w & 0xff)) {
+            // entries whose row node is not owned carry the spare pair index (never flushed)
+            const unsigned char* sb = stg + stage * SLOT;
+            const unsigned char* kb = sb + tid * 8;
+            const unsigned char* cb = sb + KB;
+            unsigned char* ab = reinterpret_cast<unsigned char*>(acc);
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                if (t < T - 1 || MM % NT == 0 || tid + NT * t < MM) {
+                    const uint32_t c = *reinterpret_cast<const uint16_t*>(cb + cio[t]);
+                    const double kv = *reinterpret_cast<const double*>(kb + t * NT * 8);
+                    double* a = reinterpret_cast<double*>(ab + c * (DD * 8) + co8[t]);
+                    *a += kv;
+                }
+            }
+        }
+        if (k == P - 1) {  // patch end: a warp per row, one RED per distinct slot
+            const int n_rows = (h.w >> 8) & 0xff;
+            if (tid < n_rows) {
+                s_rows[tid] = m_row;
+                s_rowpair[tid] = m_rowpair;
+            }
+#pragma unroll
+            for (int u = 0; u < PPT; ++u) s_pairs[tid + NT * u] = m_pair[u];
+            __syncthreads();
+            for (int r = warp; r < n_rows; r += kPatchWarps) {
+                const int64_t w = s_rows[r];
+                const int32_t rp = s_rowpair[r];  // first pair | count << 16
+                const int q0 = rp & 0xffff, cnt = rp >> 16;
+                const int64_t rowlen = w & 0xfffff;
+                double* vrow = values + (w >> 20) + fkj;
+                for (int qb = 0; qb < cnt; qb += FQ) {
+                    const int ql = qb + fq;
+                    if (fq < FQ && ql < cnt) {
+                        const int q = q0 + ql;
+                        double* dst = vrow + (s_pairs[q] & 0xff) * D;
+                        const double* src = acc + q * DD + fkj;
+#pragma unroll
+                        for (int ki = 0; ki < D; ++ki) atomicAdd(dst + ki * rowlen, src[ki * D]);
+                    }
+                }
+            }
+            __syncthreads();  // the accumulator is zeroed and the tables restaged for the next patch
+        }
+        stage = (stage + 1) % STAGES;
+        if (++k == P) {
+            k = 0;
+            pt += G;
+        }
+    }
+}
+
 // Large element blocks (hex27: m = 81, a 52 KB block per element): one CTA per element step.
 // The CTA stages only the step's row words and position bytes (double-buffered, cp.async);
 // each thread loads ALL its entries of the block straight into registers (consecutive
@@ -2262,8 +2461,38 @@ void run_atomic_cta(fea_plan* p, const double* K, double* values, cudaStream_t s
     p->last_launches += 1;
 }
 
+#ifndef FEA_PATCH_STAGES
+#define FEA_PATCH_STAGES 4
+#endif
+template <int D>
+void run_atomic_patch(fea_plan* p, const double* K, double* values, cudaStream_t s) {
+    constexpr int NPE = 8, P = kPatchElems, STAGES = FEA_PATCH_STAGES;
+    constexpr int SLOT = D * NPE * D * NPE * 8 + NPE * NPE * 2;
+    const int acc_doubles = ((p->pk_max_pairs + 1) * D * D + 1) & ~1;  // + spare pair; 16-byte aligned stages
+    const size_t smem = static_cast<size_t>(acc_doubles) * 8 + STAGES * SLOT +
+                        static_cast<size_t>(P * NPE) * 12 + static_cast<size_t>(P * NPE * NPE) * 2 + STAGES * 8;
+    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "patch accumulator too large");
+    auto kern = k_atomic_patch<D, NPE, P, STAGES>;
+    const int per_sm = launch_prep(p, kern, kPatchWarps * 32, smem);
+    const int64_t blocks = std::min<int64_t>(p->pk_n, static_cast<int64_t>(p->sms) * std::max(per_sm, 1));
+    if (blocks == 0) return;
+    kern<<<static_cast<unsigned>(blocks), kPatchWarps * 32, smem, s>>>(
+        K, p->pk_hdr.as<int4>(), p->pk_krow.as<int32_t>(), p->pk_cidx.as<uint16_t>(), p->pk_rows.as<int64_t>(),
+        p->pk_rowpair.as<int32_t>(), p->pk_pairs.as<uint16_t>(), p->pk_n, acc_doubles, values);
+    FEA_CK(cudaGetLastError());
+    p->last_launches += 1;
+}
+
 template <class PosT>
 bool atomic_staged(fea_plan* p, const double* K, double* values, cudaStream_t s) {
+    if (p->pk_n > 0 && (reinterpret_cast<uintptr_t>(K) & 15u) == 0) {  // patch pre-reduction
+        switch (p->d) {
+            case 1: run_atomic_patch<1>(p, K, values, s); return true;
+            case 2: run_atomic_patch<2>(p, K, values, s); return true;
+            case 3: run_atomic_patch<3>(p, K, values, s); return true;
+            default: break;
+        }
+    }
     if (!p->at_krow.p) return false;
     if ((reinterpret_cast<uintptr_t>(K) & 7u) == 0) {  // k_atomic_direct
         if (p->d == 3 && p->npe == 27) { run_atomic_cta<3, 27, PosT>(p, K, values, s); return true; }

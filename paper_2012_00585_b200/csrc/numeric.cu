@@ -20,6 +20,7 @@
 namespace feagpu {
 
 void build_atomic_maps(fea_plan* p, cudaStream_t s);
+void build_patches(fea_plan* p, cudaStream_t s);
 
 void ensure_element_maps(fea_plan* p, cudaStream_t s) {
     if (p->posE.p && p->order.p) return;
@@ -79,6 +80,192 @@ void ensure_element_maps(fea_plan* p, cudaStream_t s) {
         FEA_CK(cudaStreamSynchronize(s));
     }
     build_atomic_maps(p, s);
+    build_patches(p, s);
+}
+
+// Patches of k_atomic_patch (npe = 8, d <= 3, byte positions, no repeated nodes): greedy growth
+// from the atomic visit order — the first unassigned element, then repeatedly the unassigned
+// element sharing the most nodes with the patch (ties: earlier in the visit order) — up to
+// kPatchElems elements; on structured hex8 meshes this tiles 2 x 2 x 2 blocks. Per patch the
+// distinct (owned row node, column node) pairs, sorted by (row, position), and per element the
+// pair index of each (a, b). Host work, once per plan (on the first atomic assembly).
+void build_patches(fea_plan* p, cudaStream_t s) {
+    if (p->npe != 8 || p->d > 3 || p->pos_bytes != 1 || p->dup_nodes || p->E == 0 || knobs().atomic_no_patch ||
+        knobs().atomic_legacy || p->pk_n > 0)
+        return;
+    constexpr int NPE = 8, NN = 64, P = kPatchElems;
+    const int64_t E = p->E;
+    std::vector<int32_t> order(E), krow(E), conn(static_cast<size_t>(p->krows() * NPE));
+    std::vector<uint8_t> posE(static_cast<size_t>(E * NN));
+    std::vector<int64_t> nptr(static_cast<size_t>(p->n_own + 1));
+    FEA_CK(cudaMemcpyAsync(order.data(), p->order.p, E * 4, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaMemcpyAsync(krow.data(), p->elem_krow.p, E * 4, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaMemcpyAsync(conn.data(), p->conn_k.p, conn.size() * 4, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaMemcpyAsync(posE.data(), p->posE.p, posE.size(), cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaMemcpyAsync(nptr.data(), p->nptr.p, nptr.size() * 8, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaStreamSynchronize(s));
+    auto node = [&](int64_t le, int a) { return conn[static_cast<size_t>(krow[le]) * NPE + a]; };
+    int32_t max_node = 0;
+    for (int64_t le = 0; le < E; ++le)
+        for (int a = 0; a < NPE; ++a) max_node = std::max(max_node, node(le, a));
+    const int64_t nn = static_cast<int64_t>(max_node) + 1;
+    // node -> elements (local ids)
+    std::vector<int64_t> aptr(nn + 1, 0);
+    for (int64_t le = 0; le < E; ++le)
+        for (int a = 0; a < NPE; ++a) ++aptr[node(le, a) + 1];
+    for (int64_t v = 0; v < nn; ++v) aptr[v + 1] += aptr[v];
+    std::vector<int32_t> aelem(static_cast<size_t>(aptr[nn]));
+    {
+        std::vector<int64_t> fill(aptr.begin(), aptr.end() - 1);
+        for (int64_t le = 0; le < E; ++le)
+            for (int a = 0; a < NPE; ++a) aelem[fill[node(le, a)]++] = static_cast<int32_t>(le);
+    }
+    std::vector<int32_t> vpos(E);
+    for (int64_t i = 0; i < E; ++i) vpos[order[i]] = static_cast<int32_t>(i);
+    // greedy patches
+    std::vector<char> assigned(E, 0);
+    std::vector<int32_t> stamp(E, -1);
+    std::vector<int16_t> cnt(E, 0);
+    std::vector<int32_t> members;  // P per patch, -1 padded
+    members.reserve(static_cast<size_t>(E / 4 + P));
+    std::vector<int32_t> cand;
+    int32_t pid = 0;
+    for (int64_t i = 0; i < E; ++i) {
+        const int32_t e0 = order[i];
+        if (assigned[e0]) continue;
+        cand.clear();
+        int n_m = 0;
+        auto add = [&](int32_t e) {
+            assigned[e] = 1;
+            members.push_back(e);
+            ++n_m;
+            for (int a = 0; a < NPE; ++a) {
+                const int32_t v = node(e, a);
+                for (int64_t k = aptr[v]; k < aptr[v + 1]; ++k) {
+                    const int32_t g = aelem[k];
+                    if (assigned[g]) continue;
+                    if (stamp[g] != pid) {
+                        stamp[g] = pid;
+                        cnt[g] = 0;
+                        cand.push_back(g);
+                    }
+                    ++cnt[g];
+                }
+            }
+        };
+        add(e0);
+        while (n_m < P) {
+            int32_t best = -1;
+            for (int32_t g : cand)
+                if (!assigned[g] && (best < 0 || cnt[g] > cnt[best] || (cnt[g] == cnt[best] && vpos[g] < vpos[best])))
+                    best = g;
+            if (best < 0) break;
+            add(best);
+        }
+        for (; n_m < P; ++n_m) members.push_back(-1);
+        ++pid;
+    }
+    const int64_t n_patch = pid;
+    // per patch: rows, pairs, element pair indices
+    std::vector<int32_t> hk(static_cast<size_t>(n_patch * P), -1);
+    std::vector<uint16_t> hc(static_cast<size_t>(n_patch * P * NN), 0xffffu);
+    std::vector<int4> hh(static_cast<size_t>(n_patch));
+    std::vector<int64_t> hrows;
+    std::vector<int32_t> hrowpair;
+    std::vector<uint16_t> hpairs;
+    hrows.reserve(static_cast<size_t>(n_patch) * 30);
+    hpairs.reserve(static_cast<size_t>(n_patch) * 350);
+    std::vector<int32_t> nstamp(nn, -1), nrow(nn, 0);
+    std::vector<int32_t> pstamp(64 * 256, -1);
+    std::vector<uint16_t> pidx(64 * 256, 0);
+    int max_pairs = 0;
+    for (int64_t q = 0; q < n_patch; ++q) {
+        int n_rows = 0, n_el = 0;
+        std::vector<int64_t> prow;   // row node (owned, local) per row index
+        std::vector<int32_t> keys;   // row << 8 | pos per pair (insertion order)
+        uint16_t tmp[P][NN];
+        for (int k = 0; k < P; ++k) {
+            const int32_t le = members[q * P + k];
+            for (int x = 0; x < NN; ++x) tmp[k][x] = 0xffffu;
+            if (le < 0) continue;
+            ++n_el;
+            hk[q * P + k] = krow[le];
+            for (int a = 0; a < NPE; ++a) {
+                const int64_t vo = static_cast<int64_t>(node(le, a)) - p->node_begin;
+                if (vo < 0 || vo >= p->n_own) continue;
+                const int32_t v = node(le, a);
+                if (nstamp[v] != q) {
+                    nstamp[v] = static_cast<int32_t>(q);
+                    nrow[v] = n_rows++;
+                    prow.push_back(vo);
+                }
+                const int r = nrow[v];
+                for (int b = 0; b < NPE; ++b) {
+                    const int key = r * 256 + posE[static_cast<size_t>(le) * NN + a * NPE + b];
+                    if (pstamp[key] != q) {
+                        pstamp[key] = static_cast<int32_t>(q);
+                        pidx[key] = static_cast<uint16_t>(keys.size());
+                        keys.push_back(key);
+                    }
+                    tmp[k][a * NPE + b] = pidx[key];
+                }
+            }
+        }
+        // sort pairs by (row, position); remap the element indices
+        std::vector<int32_t> sorted(keys);
+        std::sort(sorted.begin(), sorted.end());
+        std::vector<uint16_t> remap(keys.size());
+        for (size_t i2 = 0; i2 < sorted.size(); ++i2) pidx[sorted[i2]] = static_cast<uint16_t>(i2);
+        for (size_t i2 = 0; i2 < keys.size(); ++i2) remap[i2] = pidx[keys[i2]];
+        for (int k = 0; k < P; ++k)
+            for (int x = 0; x < NN; ++x)
+                if (tmp[k][x] != 0xffffu) hc[(q * P + k) * NN + x] = remap[tmp[k][x]];
+        FEA_REQUIRE(hpairs.size() + sorted.size() < (size_t{1} << 31) && n_rows < 256, FEA_ERR_INVALID,
+                    "internal: patch tables too large");
+        hh[q] = make_int4(0, static_cast<int>(hpairs.size()), static_cast<int>(hrows.size()),
+                          n_el | (n_rows << 8) | (static_cast<int>(sorted.size()) << 16));
+        for (int64_t vo : prow) {
+            const int64_t c0 = nptr[vo];
+            hrows.push_back(((static_cast<int64_t>(p->d) * p->d * c0) << 20) |
+                            (static_cast<int64_t>(p->d) * (nptr[vo + 1] - c0)));
+        }
+        {  // first pair and pair count per row (pairs sorted by row index)
+            std::vector<int32_t> first(prow.size(), 0), count(prow.size(), 0);
+            for (size_t i2 = 0; i2 < sorted.size(); ++i2) {
+                const int r = sorted[i2] >> 8;
+                if (count[r]++ == 0) first[r] = static_cast<int32_t>(i2);
+            }
+            for (size_t r = 0; r < prow.size(); ++r) hrowpair.push_back(first[r] | (count[r] << 16));
+        }
+        for (int32_t key : sorted) hpairs.push_back(static_cast<uint16_t>(((key >> 8) << 8) | (key & 0xff)));
+        max_pairs = std::max<int>(max_pairs, static_cast<int>(sorted.size()));
+    }
+    // entries of a row node outside the owned range add into the spare pair (index max_pairs,
+    // allocated by the kernel and never flushed): no branch per entry in the kernel
+    for (int64_t q = 0; q < n_patch; ++q) {
+        const int n_el = hh[q].w & 0xff;
+        for (int k = 0; k < n_el; ++k)
+            for (int x = 0; x < NN; ++x) {
+                uint16_t& c = hc[(q * P + k) * NN + x];
+                if (c == 0xffffu) c = static_cast<uint16_t>(max_pairs);
+            }
+    }
+    p->pk_hdr.alloc(std::max<int64_t>(n_patch, 1) * 16);
+    p->pk_krow.alloc(hk.size() * 4);
+    p->pk_cidx.alloc(hc.size() * 2);
+    p->pk_rows.alloc(std::max<size_t>(hrows.size(), 1) * 8);
+    p->pk_pairs.alloc(std::max<size_t>(hpairs.size(), 1) * 2);
+    p->pk_rowpair.alloc(std::max<size_t>(hrowpair.size(), 1) * 4);
+    if (!hrowpair.empty())
+        FEA_CK(cudaMemcpyAsync(p->pk_rowpair.p, hrowpair.data(), hrowpair.size() * 4, cudaMemcpyHostToDevice, s));
+    FEA_CK(cudaMemcpyAsync(p->pk_hdr.p, hh.data(), hh.size() * 16, cudaMemcpyHostToDevice, s));
+    FEA_CK(cudaMemcpyAsync(p->pk_krow.p, hk.data(), hk.size() * 4, cudaMemcpyHostToDevice, s));
+    FEA_CK(cudaMemcpyAsync(p->pk_cidx.p, hc.data(), hc.size() * 2, cudaMemcpyHostToDevice, s));
+    if (!hrows.empty()) FEA_CK(cudaMemcpyAsync(p->pk_rows.p, hrows.data(), hrows.size() * 8, cudaMemcpyHostToDevice, s));
+    if (!hpairs.empty()) FEA_CK(cudaMemcpyAsync(p->pk_pairs.p, hpairs.data(), hpairs.size() * 2, cudaMemcpyHostToDevice, s));
+    FEA_CK(cudaStreamSynchronize(s));
+    p->pk_max_pairs = max_pairs;
+    p->pk_n = n_patch;
 }
 
 // Visit-order metadata of k_atomic_staged (shapes d <= 3, npe in {4, 8}); other shapes, and

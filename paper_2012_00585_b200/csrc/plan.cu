@@ -67,7 +67,7 @@ const Knobs& knobs() {
             const char* e = std::getenv(n);
             return e ? (std::atoi(e) & 15) : -1;
         };
-        return Knobs{on("FEA_ATOMIC_LEGACY"), on("FEA_SLOT_NO_FIXED"),   on("FEA_CN_UNPACKED"),
+        return Knobs{on("FEA_ATOMIC_LEGACY"), on("FEA_ATOMIC_NO_PATCH"), on("FEA_SLOT_NO_FIXED"), on("FEA_CN_UNPACKED"),
                      on("FEA_CN_NO_RECORDS"), on("FEA_D1_NO_DIRECT"),    on("FEA_D1_NO_VEC"),
                      mod("FEA_D1_ACC_STRIDE_MOD16"), mod("FEA_D1V_ACC_STRIDE_MOD16")};
     }();
@@ -1122,7 +1122,9 @@ int64_t metadata_bytes(const fea_plan* p) {
                                 p->order.bytes + p->at_krow.bytes + p->at_rows.bytes + p->at_pos.bytes + p->colour_elems.bytes + p->adjC.bytes + p->posAC.bytes +
                                 p->node_order.bytes + p->trav_ptr.bytes + p->trav_meta.bytes +
                                 p->trav_rec.bytes + p->trav_recC.bytes + p->cnr_hdr.bytes + p->cnr_rec.bytes +
-                                p->cnr_recC.bytes + p->slot_hdr.bytes + p->slot_rec.bytes + p->slot_recC.bytes);
+                                p->cnr_recC.bytes + p->slot_hdr.bytes + p->slot_rec.bytes + p->slot_recC.bytes +
+                                p->pk_hdr.bytes + p->pk_krow.bytes + p->pk_cidx.bytes + p->pk_rows.bytes + p->pk_rowpair.bytes +
+                                p->pk_pairs.bytes);
 }
 
 }  // namespace feagpu
