@@ -147,6 +147,14 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// Programmatic dependent launch: a kernel launched with the PDL attribute may start while the
+// previous kernel of its stream is still running; it reads only plan metadata (constant for the
+// plan) before pdl_wait(), and K / values (which the previous kernel may have written) after.
+// Without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 #ifndef FEA_GATHER_MIN_BLOCKS
 #define FEA_GATHER_MIN_BLOCKS 5
@@ -1023,6 +1031,14 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_D1V_MINB)
 #ifndef FEA_D1G_U
 #define FEA_D1G_U 8  // records + K rows in flight per lane; cfg3: 4 -> 0.620 ms, 8 -> 0.614
 #endif
+#ifndef FEA_D1G_KLOAD
+#define FEA_D1G_KLOAD 0  // K row loads: 0 L2 only (.cg), 1 read-only path (.nc, L1), 2 L1 (.ca)
+#endif
+__device__ __forceinline__ double kload_d1(const double* p) {
+    if (FEA_D1G_KLOAD == 1) return __ldg(p);
+    if (FEA_D1G_KLOAD == 2) return __ldca(p);
+    return __ldcg(p);
+}
 template <int U>
 __global__ void __launch_bounds__(kWarps * 32)
     k_gather_d1g(const double* __restrict__ K, int64_t n_own, int acc_stride, int accumulate,
@@ -1038,24 +1054,29 @@ __global__ void __launch_bounds__(kWarps * 32)
     const int64_t t = static_cast<int64_t>(blockIdx.x) * kWarps * GPW + grp;
     int64_t a0 = 0, vb = 0;
     int n = 0, rl = 0;
-    if (t < n_own) {
+    if (t < n_own) {  // plan metadata: may run ahead of the previous kernel's end (PDL)
         a0 = tptr[t];
         n = static_cast<int>(tptr[t + 1] - a0);
         const int64_t mt = tmeta[t];
         vb = mt >> 20;
         rl = static_cast<int>(mt & 0xfffff);
     }
-    for (int i = gl; i < rl; i += G) acc[i] = accumulate ? values[vb + i] : 0.0;
     const int n_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
     const int2* src = trec + a0;
+    int2 r0[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r0[u] = u < n ? __ldg(src + u) : make_int2(0, 0);
+    pdl_wait();  // K and values only after the previous kernel of the stream has finished
+    pdl_launch_dependents();
+    for (int i = gl; i < rl; i += G) acc[i] = accumulate ? values[vb + i] : 0.0;
     for (int k0 = 0; k0 < n_max; k0 += U) {
         int2 r[U];
         double kv[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) r[u] = k0 + u < n ? __ldg(src + k0 + u) : make_int2(0, 0);
+        for (int u = 0; u < U; ++u) r[u] = k0 == 0 ? r0[u] : (k0 + u < n ? __ldg(src + k0 + u) : make_int2(0, 0));
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            kv[u] = k0 + u < n ? __ldcg(K + static_cast<int64_t>(r[u].x) * 4 + gl) : 0.0;
+            kv[u] = k0 + u < n ? kload_d1(K + static_cast<int64_t>(r[u].x) * 4 + gl) : 0.0;
         __syncwarp();
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -1998,6 +2019,31 @@ int launch_prep(fea_plan* p, F* kern, int threads, size_t smem) {
     return per_sm;
 }
 
+#ifndef FEA_PDL
+#define FEA_PDL 1
+#endif
+// Launch with the programmatic-dependent-launch attribute (FEA_PDL): back-to-back assemblies on
+// one stream (or in a CUDA graph) overlap the next kernel's launch and metadata prologue with
+// the previous kernel's tail. Kernels launched this way call pdl_wait() before K / values.
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s, Args... args) {
+    if (!FEA_PDL) {
+        kern<<<grid, block, smem, s>>>(args...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    FEA_CK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 // Traversal window of a windowed gather launch (fea_plan::win_t0 / win_n).
 struct Win {
     int64_t t0, n;
@@ -2301,9 +2347,9 @@ void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* v
         const Win wn = window_of(p);
         const int64_t blocks_w = (wn.n + per_cta - 1) / per_cta;
         if (blocks_w == 0) return;
-        kg<<<static_cast<unsigned>(blocks_w), kWarps * 32, smemg, s>>>(
-            K, wn.n, acc_stride, accumulate ? 1 : 0, p->trav_ptr.as<int64_t>() + wn.t0,
-            p->trav_meta.as<int64_t>() + wn.t0, reinterpret_cast<const int2*>(recs.as<int32_t>()), values);
+        launch_pdl(kg, static_cast<unsigned>(blocks_w), kWarps * 32, smemg, s, K, wn.n, acc_stride,
+                   accumulate ? 1 : 0, p->trav_ptr.as<int64_t>() + wn.t0, p->trav_meta.as<int64_t>() + wn.t0,
+                   reinterpret_cast<const int2*>(recs.as<int32_t>()), values);
         FEA_CK(cudaGetLastError());
         p->last_launches += 1;
         return;

@@ -780,7 +780,7 @@ __global__ void k_trav_count(const int32_t* __restrict__ order, const int64_t* _
                              int64_t* __restrict__ meta) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_own;
          t += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t v = order[t];
+        const int64_t v = order != nullptr ? order[t] : t;
         cnt[t] = adj_ptr[v + 1] - adj_ptr[v];
         meta[t] = (nptr[v] << 20) | (nptr[v + 1] - nptr[v]);
     }
@@ -794,7 +794,7 @@ __global__ void k_trav_records(const int32_t* __restrict__ order, const int64_t*
     const int lane = threadIdx.x & 31;
     for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n_own;
          t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int32_t v = order[t];
+        const int64_t v = order != nullptr ? order[t] : t;
         const int64_t a0 = adj_ptr[v], n = adj_ptr[v + 1] - a0, r0 = tptr[t];
         for (int64_t k = lane; k < n; k += 32) {
             int32_t* r = rec + (r0 + k) * rw;
@@ -810,8 +810,9 @@ void build_traversal(fea_plan* p, cudaStream_t s) {
     p->trav_ptr.reset();
     p->trav_meta.reset();
     p->trav_rec.reset();
-    if (!p->node_order.p || p->d != 1 || p->npe > 32 || p->d1_disabled || std::getenv("FEA_NO_TRAVERSAL_RECORDS"))
-        return;
+    // (also without a traversal order: the records then follow node id order and the d = 1
+    // kernels still save the adj_ptr -> adj / posA round trip per node, cfg1)
+    if (p->d != 1 || p->npe > 32 || p->d1_disabled || std::getenv("FEA_NO_TRAVERSAL_RECORDS")) return;
     const int pw = p->pstride * p->pos_bytes / 4;
     const int rw = pw == 1 ? 2 : (pw + 4) & ~3;
     DevBuf cnt;

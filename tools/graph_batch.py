@@ -28,6 +28,8 @@ ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--buffers", type=int, default=16)
 ap.add_argument("--replays", type=int, default=5)
 ap.add_argument("--strategies", default="sorted,atomic")
+ap.add_argument("--branches", type=int, default=1,
+                help="independent assemblies run as this many parallel graph branches (fork/join on events)")
 a = ap.parse_args()
 
 for cfg in (int(c) for c in a.configs.split(",")):
@@ -40,7 +42,7 @@ for cfg in (int(c) for c in a.configs.split(",")):
     Ks = [fea.fill_seeded_k(E, m, 42 + i) for i in range(nb)]
     Vs = [torch.zeros(plan.nnz, dtype=torch.float64, device="cuda") for _ in range(nb)]
     alg = 8 * E * m * m + 8 * plan.nnz + 4 * E * npe
-    out = {"config": cfg, "elements": E, "m": m, "nnz": plan.nnz, "algorithmic_bytes": alg,
+    out = {"config": cfg, "branches": a.branches, "elements": E, "m": m, "nnz": plan.nnz, "algorithmic_bytes": alg,
            "working_set_bytes": nb * (8 * E * m * m + 8 * plan.nnz), "batch": a.batch, "strategies": {}}
     s = torch.cuda.Stream()
     for strategy in a.strategies.split(","):
@@ -49,11 +51,20 @@ for cfg in (int(c) for c in a.configs.split(",")):
             plan.assemble(Ks[0], Vs[0], strategy=strategy, accumulate=acc, stream=s)  # lazy tables
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
+        side = [torch.cuda.Stream() for _ in range(a.branches)]
         with torch.cuda.graph(g, stream=s):
-            for i in range(a.batch):
-                if acc:
-                    Vs[i % nb].zero_()
-                plan.assemble(Ks[i % nb], Vs[i % nb], strategy=strategy, accumulate=acc, stream=s)
+            fork = torch.cuda.Event()
+            fork.record(s)
+            for b, ss in enumerate(side):  # branch b: assemblies b, b + branches, ...
+                ss.wait_event(fork)
+                with torch.cuda.stream(ss):
+                    for i in range(b, a.batch, a.branches):
+                        if acc:
+                            Vs[i % nb].zero_()
+                        plan.assemble(Ks[i % nb], Vs[i % nb], strategy=strategy, accumulate=acc, stream=ss)
+                join = torch.cuda.Event()
+                join.record(ss)
+                s.wait_event(join)
         with torch.cuda.stream(s):  # replay() launches on the current stream
             g.replay()
             torch.cuda.synchronize()
