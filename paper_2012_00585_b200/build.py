@@ -36,7 +36,8 @@ def build(verbose: bool = False, force: bool = False, out: Path | None = None,
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "fea_gpu.h"]
     if not force and not _stale(lib, deps):
         return lib
-    objdir = PKG / ("_build" if out is None else "_build_" + lib.stem)
+    # variant objects live next to the variant library (variants/ is not shipped to the GPU box)
+    objdir = PKG / "_build" if out is None else lib.parent / ("_obj_" + lib.stem)
     objdir.mkdir(exist_ok=True)
     from concurrent.futures import ThreadPoolExecutor
 

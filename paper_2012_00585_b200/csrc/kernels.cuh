@@ -1039,8 +1039,11 @@ __device__ __forceinline__ double kload_d1(const double* p) {
     if (FEA_D1G_KLOAD == 2) return __ldca(p);
     return __ldcg(p);
 }
+#ifndef FEA_D1G_MINB
+#define FEA_D1G_MINB 1
+#endif
 template <int U>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, FEA_D1G_MINB)
     k_gather_d1g(const double* __restrict__ K, int64_t n_own, int acc_stride, int accumulate,
                  const int64_t* __restrict__ tptr, const int64_t* __restrict__ tmeta,
                  const int2* __restrict__ trec, double* __restrict__ values) {
@@ -1063,9 +1066,12 @@ __global__ void __launch_bounds__(kWarps * 32)
     }
     const int n_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
     const int2* src = trec + a0;
+#ifndef FEA_D1G_PREFETCH
+#define FEA_D1G_PREFETCH 0  // first record batch loaded before the PDL wait (+25 registers)
+#endif
     int2 r0[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) r0[u] = u < n ? __ldg(src + u) : make_int2(0, 0);
+    for (int u = 0; u < U; ++u) r0[u] = FEA_D1G_PREFETCH && u < n ? __ldg(src + u) : make_int2(0, 0);
     pdl_wait();  // K and values only after the previous kernel of the stream has finished
     pdl_launch_dependents();
     for (int i = gl; i < rl; i += G) acc[i] = accumulate ? values[vb + i] : 0.0;
@@ -1073,7 +1079,8 @@ __global__ void __launch_bounds__(kWarps * 32)
         int2 r[U];
         double kv[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) r[u] = k0 == 0 ? r0[u] : (k0 + u < n ? __ldg(src + k0 + u) : make_int2(0, 0));
+        for (int u = 0; u < U; ++u)
+            r[u] = (FEA_D1G_PREFETCH && k0 == 0) ? r0[u] : (k0 + u < n ? __ldg(src + k0 + u) : make_int2(0, 0));
 #pragma unroll
         for (int u = 0; u < U; ++u)
             kv[u] = k0 + u < n ? kload_d1(K + static_cast<int64_t>(r[u].x) * 4 + gl) : 0.0;
