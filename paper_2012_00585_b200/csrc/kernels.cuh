@@ -1707,6 +1707,8 @@ __global__ void __launch_bounds__(kPatchWarps * 32)
         mbar_fence_init();
     }
     __syncthreads();
+    // K is read once: L2 evict-first for its bulk copies keeps the values lines being reduced
+    // into resident (created per copy: a hoisted createpolicy was miscompiled, see above)
     // issue cursor (STAGES - 1 element slots ahead of the fold): patch and slot. Thread 0
     // copies a slot's K block (4.6 KB contiguous) and its pair indices with two bulk copies.
     int64_t ipt = blockIdx.x;
@@ -1724,7 +1726,9 @@ __global__ void __launch_bounds__(kPatchWarps * 32)
             unsigned char* sb = stg + stage * SLOT;
             fence_proxy_async_smem();  // the stage was last read by generic loads
             mbar_arrive_expect_tx(bar, SLOT);
-            bulk_g2s(smem_u32(sb), K + static_cast<int64_t>(kr) * MM, KB, bar);
+            if (FEA_PATCH_K_HINT)
+                tma_load_1d(smem_u32(sb), K + static_cast<int64_t>(kr) * MM, KB, bar, policy_evict_first());
+            else bulk_g2s(smem_u32(sb), K + static_cast<int64_t>(kr) * MM, KB, bar);
             bulk_g2s(smem_u32(sb + KB), pk_cidx + (ipt * P + ik) * NN, CB, bar);
         } else {
             mbar_arrive(bar);  // empty slot: complete the phase without data
