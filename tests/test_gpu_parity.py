@@ -652,3 +652,22 @@ def test_binding_rejects_bad_buffers(gpu):
             plan.assemble_host(good.cpu().numpy().astype(np.float32))
         with pytest.raises(AssertionError):
             plan.assemble_seeded(1, v[:-1])
+
+
+def test_pinned_host_buffers_end_to_end(gpu, orc):
+    """hostmem.pinned_empty (cudaHostRegister'ed numpy arrays) through the pipelined host path:
+    bit-exact vs the oracle; the registration is dropped with the array."""
+    import gc
+    from paper_2012_00585_b200.hostmem import pinned_empty
+    conn, nn, ed, n_rows = problem("hex8", 5, 3, None)
+    P = orc.Pattern.build(conn, nn, 3)
+    E, m = ed.shape
+    Kh = pinned_empty((E, m, m))
+    Kh[...] = orc.fill_k(11, E, m)
+    vh = pinned_empty((P.nnz,))
+    with gpu.Plan(ed, n_rows, dofs_per_node=3) as plan:
+        plan.set_host_windows(4)
+        plan.assemble_host(Kh, vh, strategy="sorted")
+        assert vh.tobytes() == P.assemble_sequential(ed, Kh).tobytes()
+    del Kh, vh
+    gc.collect()
