@@ -244,6 +244,21 @@ FEA_API fea_status fea_plan_spmv(const fea_plan* plan, const double* values, con
                                  void* stream);
 
 /*
+ * The device primitives of the symbolic phase (north-star subsystem 1: sort/unique + exclusive
+ * scan; pattern.cpp:24-108 does the same job with std::sort / std::unique per row). Hand-written
+ * (csrc/prims.cu), exposed so the tests can pin them and so callers that build their own
+ * patterns can reuse them. All pointers are DEVICE pointers; stream-ordered, return after the
+ * work has completed.
+ *  fea_exclusive_sum_i64: out[i] = in[0] + ... + in[i-1] (in and out may be the same array)
+ *  fea_sort_pairs_u32   : stable LSD radix sort of (uint32 key, int32 value) pairs by key bits
+ *                         [begin_bit, end_bit); inputs intact, n < 2^31
+ */
+FEA_API fea_status fea_exclusive_sum_i64(const int64_t* in, int64_t* out, int64_t n, void* stream);
+FEA_API fea_status fea_sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const int32_t* vals_in,
+                                      int32_t* vals_out, int64_t n, int32_t begin_bit, int32_t end_bit,
+                                      void* stream);
+
+/*
  * Peer memory for the fused row-partitioned assembly + gather (no reference
  * counterpart — the reference is shared-memory only). The root exports its global
  * values buffer, every rank maps it and fea_assemble()s its owned row block straight into it at

@@ -63,6 +63,8 @@ SIGNATURES = {
     "fea_spmv_csr": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "fea_spmv_crac": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "fea_plan_spmv": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "fea_exclusive_sum_i64": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "fea_sort_pairs_u32": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_int32, c_void_p]),
     "fea_ipc_export": (c_int, [c_void_p, c_void_p, _P64]),
     "fea_ipc_open": (c_int, [c_void_p, c_int, POINTER(c_void_p)]),
     "fea_ipc_close": (c_int, [c_void_p]),

@@ -335,6 +335,30 @@ def fill_seeded_k(n: int, m: int, seed: int, elem_ids=None, device: int = 0, out
     return out
 
 
+def exclusive_sum(x, out=None, stream=None):
+    """Exclusive prefix sum of a device int64 tensor (the symbolic phase's own scan, csrc/prims.cu)."""
+    import torch
+    if x.dtype != torch.int64 or not x.is_cuda or not x.is_contiguous():
+        raise ValueError("exclusive_sum takes a contiguous CUDA int64 tensor")
+    if out is None:
+        out = torch.empty_like(x)
+    _check(N.lib().fea_exclusive_sum_i64(_ptr(x), _ptr(out), x.numel(), _stream_ptr(stream, x.device.index)))
+    return out
+
+
+def sort_pairs(keys, vals, begin_bit: int = 0, end_bit: int = 32, stream=None):
+    """Stable LSD radix sort of (uint32-valued keys, int32 vals) device pairs by key bits
+    [begin_bit, end_bit) (csrc/prims.cu). keys: int32/uint32-width CUDA tensor (bit pattern)."""
+    import torch
+    if keys.element_size() != 4 or vals.dtype != torch.int32 or not keys.is_cuda or keys.numel() != vals.numel():
+        raise ValueError("sort_pairs takes 4-byte CUDA keys and int32 values of equal length")
+    keys, vals = keys.contiguous(), vals.contiguous()
+    ko, vo = torch.empty_like(keys), torch.empty_like(vals)
+    _check(N.lib().fea_sort_pairs_u32(_ptr(keys), _ptr(ko), _ptr(vals), _ptr(vo), keys.numel(), begin_bit,
+                                      end_bit, _stream_ptr(stream, keys.device.index)))
+    return ko, vo
+
+
 def spmv_csr(row_ptr, cols, values, x, y=None, stream=None):
     """y = A x over device CSR arrays (int64 row_ptr/cols, fp64 values/x)."""
     import torch

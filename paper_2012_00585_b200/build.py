@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libfea_gpu.so"
-SOURCES = ["plan.cu", "numeric.cu", "gather_u8.cu", "gather_u16.cu", "spmv.cu", "peer.cu"]
+SOURCES = ["plan.cu", "numeric.cu", "gather_u8.cu", "gather_u16.cu", "spmv.cu", "peer.cu", "prims.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-fvisibility=hidden", "-Xptxas", "-v",

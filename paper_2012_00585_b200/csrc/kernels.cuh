@@ -2,7 +2,6 @@
 // position-type instantiation units gather_u8.cu / gather_u16.cu; everything here is
 // TU-local, see numeric.cu for the design notes of every kernel).
 #pragma once
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cstring>
@@ -10,6 +9,7 @@
 #include <string>
 
 #include "internal.cuh"
+#include "prims.cuh"
 
 namespace feagpu {
 extern thread_local std::string g_err;
@@ -1988,15 +1988,6 @@ __global__ void k_fill_k(double* __restrict__ K, int64_t n, int m, uint64_t seed
         const int i = rem / m, j = rem - (rem / m) * m;
         K[t] = kval(seed, ids ? ids[e] : e, i, j);
     }
-}
-
-template <class F>
-void cub_call(F&& f) {
-    size_t tb = 0;
-    FEA_CK(f(nullptr, tb));
-    DevBuf t;
-    t.alloc(tb);
-    FEA_CK(f(t.p, tb));
 }
 
 // --- launch helpers --------------------------------------------------------

@@ -70,11 +70,8 @@ void ensure_element_maps(fea_plan* p, cudaStream_t s) {
         if (2 * static_cast<int64_t>(shared) >= p->E - 1) {
             k_iota32<<<grid_for(p->E, 256), 256, 0, s>>>(p->order.as<int32_t>(), p->E);
         } else {
-            cub_call([&](void* t, size_t& tb) {
-                return cub::DeviceRadixSort::SortPairs(t, tb, keys.as<uint32_t>(),
-                                                       keys2.as<uint32_t>(), vals.as<int32_t>(),
-                                                       p->order.as<int32_t>(), (int)p->E, 0, 32, s);
-            });
+            radix_sort_pairs(keys.as<uint32_t>(), keys2.as<uint32_t>(), vals.as<int32_t>(),
+                             p->order.as<int32_t>(), p->E, 0, 32, s);
         }
         FEA_CK(cudaGetLastError());
         FEA_CK(cudaStreamSynchronize(s));
@@ -651,6 +648,25 @@ fea_status fea_fill_seeded_k(double* K, int64_t n, int32_t m, uint64_t seed,
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         k_fill_k<<<grid_for(n * m * m, 256), 256, 0, s>>>(K, n, m, seed, elem_ids);
         FEA_CK(cudaGetLastError());
+    });
+}
+
+fea_status fea_exclusive_sum_i64(const int64_t* in, int64_t* out, int64_t n, void* stream) {
+    return guarded_n([&] {
+        FEA_REQUIRE(n >= 0 && (n == 0 || (in && out)), FEA_ERR_INVALID, "bad arguments");
+        exclusive_sum(in, out, n, static_cast<cudaStream_t>(stream));
+        FEA_CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    });
+}
+
+fea_status fea_sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const int32_t* vals_in,
+                              int32_t* vals_out, int64_t n, int32_t begin_bit, int32_t end_bit, void* stream) {
+    return guarded_n([&] {
+        FEA_REQUIRE(n >= 0 && (n == 0 || (keys_in && keys_out && vals_in && vals_out)) && begin_bit >= 0 &&
+                        end_bit <= 32 && begin_bit <= end_bit,
+                    FEA_ERR_INVALID, "bad arguments");
+        radix_sort_pairs(keys_in, keys_out, vals_in, vals_out, n, begin_bit, end_bit,
+                         static_cast<cudaStream_t>(stream));
     });
 }
 

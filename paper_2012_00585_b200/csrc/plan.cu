@@ -17,15 +17,16 @@
 // so the slot map is one small row-relative position per (element, node a,
 // node b) — uint8 when every node row has <= 256 neighbour nodes — instead of
 // an int32/int64 slot per element-matrix entry.
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <numeric>
 #include <string>
 
 #include "internal.cuh"
+#include "prims.cuh"
 
 namespace feagpu {
 
@@ -106,15 +107,6 @@ bool is_device_ptr(const void* ptr) {
         return false;
     }
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
-}
-
-template <class F>
-void cub_call(F&& f) {
-    size_t tb = 0;
-    FEA_CK(f(nullptr, tb));
-    DevBuf t;
-    t.alloc(tb);
-    FEA_CK(f(t.p, tb));
 }
 
 unsigned grid_for(int64_t n, int threads) {
@@ -681,17 +673,11 @@ void build_adjacency(fea_plan* p, cudaStream_t s) {
             counts_b.as<unsigned long long>());
         FEA_CK(cudaGetLastError());
         const int end_bit = bits_for(static_cast<uint64_t>(p->n_own));
-        cub_call([&](void* t, size_t& tb) {
-            return cub::DeviceRadixSort::SortPairs(t, tb, keys_in.as<uint32_t>(),
-                                                   keys_out.as<uint32_t>(), vals_in.as<int32_t>(),
-                                                   vals_out.as<int32_t>(), (int)items, 0, end_bit, s);
-        });
+        radix_sort_pairs(keys_in.as<uint32_t>(), keys_out.as<uint32_t>(), vals_in.as<int32_t>(),
+                         vals_out.as<int32_t>(), items, 0, end_bit, s);
     }
     p->adj_ptr.alloc((p->n_own + 1) * sizeof(int64_t));
-    cub_call([&](void* t, size_t& tb) {
-        return cub::DeviceScan::ExclusiveSum(t, tb, counts_b.as<int64_t>(), p->adj_ptr.as<int64_t>(),
-                                             (int)(p->n_own + 1), s);
-    });
+    exclusive_sum(counts_b.as<int64_t>(), p->adj_ptr.as<int64_t>(), p->n_own + 1, s);
     FEA_CK(cudaMemcpyAsync(&p->n_adj, p->adj_ptr.as<int64_t>() + p->n_own, sizeof(int64_t),
                            cudaMemcpyDeviceToHost, s));
     FEA_CK(cudaStreamSynchronize(s));
@@ -720,10 +706,7 @@ void build_adjacency(fea_plan* p, cudaStream_t s) {
 
 void finish_counts(fea_plan* p, DevBuf& counts, cudaStream_t s) {
     p->nptr.alloc((p->n_own + 1) * sizeof(int64_t));
-    cub_call([&](void* t, size_t& tb) {
-        return cub::DeviceScan::ExclusiveSum(t, tb, counts.as<int64_t>(), p->nptr.as<int64_t>(),
-                                             (int)(p->n_own + 1), s);
-    });
+    exclusive_sum(counts.as<int64_t>(), p->nptr.as<int64_t>(), p->n_own + 1, s);
     DevBuf mx;
     mx.alloc(8);
     FEA_CK(cudaMemsetAsync(mx.p, 0, 8, s));
@@ -767,11 +750,8 @@ void build_node_order(fea_plan* p, cudaStream_t s) {
     FEA_CK(cudaStreamSynchronize(s));
     if (2 * static_cast<int64_t>(shared) >= p->n_own - 1) return;
     p->node_order.alloc(p->n_own * 4);
-    cub_call([&](void* t, size_t& tb) {
-        return cub::DeviceRadixSort::SortPairs(t, tb, keys.as<uint32_t>(), keys2.as<uint32_t>(),
-                                               vals.as<int32_t>(), p->node_order.as<int32_t>(),
-                                               (int)p->n_own, 0, 32, s);
-    });
+    radix_sort_pairs(keys.as<uint32_t>(), keys2.as<uint32_t>(), vals.as<int32_t>(),
+                     p->node_order.as<int32_t>(), p->n_own, 0, 32, s);
     FEA_CK(cudaStreamSynchronize(s));
 }
 
@@ -824,10 +804,7 @@ void build_traversal(fea_plan* p, cudaStream_t s) {
                                                          p->trav_meta.as<int64_t>());
     FEA_CK(cudaGetLastError());
     p->trav_ptr.alloc((p->n_own + 1) * 8);
-    cub_call([&](void* t, size_t& tb) {
-        return cub::DeviceScan::ExclusiveSum(t, tb, cnt.as<int64_t>(), p->trav_ptr.as<int64_t>(),
-                                             (int)(p->n_own + 1), s);
-    });
+    exclusive_sum(cnt.as<int64_t>(), p->trav_ptr.as<int64_t>(), p->n_own + 1, s);
     p->trav_rec.alloc(std::max<int64_t>(p->n_adj, 1) * rw * 4);
     k_trav_records<<<grid_for(p->n_own * 32, 256), 256, 0, s>>>(
         p->node_order.as<int32_t>(), p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(),
@@ -848,10 +825,7 @@ void build_runs(fea_plan* p, cudaStream_t s) {
                                                             runs.as<int64_t>());
     FEA_CK(cudaGetLastError());
     p->nrun_ptr.alloc((p->n_own + 1) * sizeof(int64_t));
-    cub_call([&](void* t, size_t& tb) {
-        return cub::DeviceScan::ExclusiveSum(t, tb, runs.as<int64_t>(), p->nrun_ptr.as<int64_t>(),
-                                             (int)(p->n_own + 1), s);
-    });
+    exclusive_sum(runs.as<int64_t>(), p->nrun_ptr.as<int64_t>(), p->n_own + 1, s);
     int64_t nr = 0;
     FEA_CK(cudaMemcpyAsync(&nr, p->nrun_ptr.as<int64_t>() + p->n_own, 8, cudaMemcpyDeviceToHost, s));
     FEA_CK(cudaStreamSynchronize(s));
@@ -979,10 +953,7 @@ void build_elements(fea_plan* p, const int64_t* elem_dofs, int32_t d_hint, cudaS
             k_keep_flags<<<grid_for(p->E_in, 256), 256, 0, s>>>(
                 conn_all.as<int32_t>(), p->E_in, p->npe, p->node_begin, p->node_end,
                 keep.as<int64_t>());
-        cub_call([&](void* t, size_t& tb) {
-            return cub::DeviceScan::ExclusiveSum(t, tb, keep.as<int64_t>(), pos.as<int64_t>(),
-                                                 (int)(p->E_in + 1), s);
-        });
+        exclusive_sum(keep.as<int64_t>(), pos.as<int64_t>(), p->E_in + 1, s);
         FEA_CK(cudaMemcpyAsync(&p->E, pos.as<int64_t>() + p->E_in, 8, cudaMemcpyDeviceToHost, s));
         FEA_CK(cudaStreamSynchronize(s));
         p->elem_id.alloc(p->E * 8);
@@ -1082,16 +1053,14 @@ void build_colour_incidences(fea_plan* p, const std::vector<int32_t>& colour_of_
     k_colour_keys<<<grid_for(n, 256), 256, 0, s>>>(p->adj.as<int32_t>(), n, p->npe, d_ck.as<int32_t>(),
                                                    k1.as<uint32_t>(), v1.as<int32_t>());
     FEA_CK(cudaGetLastError());
-    cub_call([&](void* t, size_t& tb) {  // pass 1: stable by colour
-        return cub::DeviceRadixSort::SortPairs(t, tb, k1.as<uint32_t>(), k2.as<uint32_t>(), v1.as<int32_t>(),
-                                               v2.as<int32_t>(), (int)n, 0, bits_for(static_cast<uint64_t>(nc)), s);
-    });
+    // pass 1: stable by colour
+    radix_sort_pairs(k1.as<uint32_t>(), k2.as<uint32_t>(), v1.as<int32_t>(), v2.as<int32_t>(), n, 0,
+                     bits_for(static_cast<uint64_t>(nc)), s);
     k_gather_keys<<<grid_for(n, 256), 256, 0, s>>>(node_of.as<int32_t>(), v2.as<int32_t>(), n, k1.as<uint32_t>());
     FEA_CK(cudaGetLastError());
-    cub_call([&](void* t, size_t& tb) {  // pass 2: stable by node
-        return cub::DeviceRadixSort::SortPairs(t, tb, k1.as<uint32_t>(), k2.as<uint32_t>(), v2.as<int32_t>(),
-                                               v1.as<int32_t>(), (int)n, 0, bits_for(static_cast<uint64_t>(p->n_own)), s);
-    });
+    // pass 2: stable by node
+    radix_sort_pairs(k1.as<uint32_t>(), k2.as<uint32_t>(), v2.as<int32_t>(), v1.as<int32_t>(), n, 0,
+                     bits_for(static_cast<uint64_t>(p->n_own)), s);
     k_permute_incidences<<<grid_for(n, 256), 256, 0, s>>>(v1.as<int32_t>(), n, row_bytes, p->adj.as<int32_t>(),
                                                           p->posA.as<unsigned char>(), p->adjC.as<int32_t>(),
                                                           p->posAC.as<unsigned char>());
