@@ -111,8 +111,16 @@ class Plan:
         """Plan against a caller-supplied CSR (row_ptr, cols) or CRAC (row_ptr, col_align) pattern."""
         lib = N.lib()
         dofs, E, m = _as_int64_dofs(elem_dofs)
-        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
-        ix = np.ascontiguousarray(idx, dtype=np.int64)
+
+        def arr(x):  # host arrays like the reference's, or device tensors used in place
+            if hasattr(x, "is_cuda"):
+                import torch
+                assert x.is_cuda and x.dtype == torch.int64 and x.is_contiguous(), \
+                    "device pattern arrays must be contiguous cuda int64 tensors"
+                return x
+            return np.ascontiguousarray(x, dtype=np.int64)
+
+        rp, ix = arr(row_ptr), arr(idx)
         f = N.FEA_FORMAT_CSR if fmt == "csr" else N.FEA_FORMAT_CRAC
         h = c_void_p(0)
         _check(lib.fea_plan_create_with_pattern(device, _ptr(dofs), E, m, n_rows, f, _ptr(rp),

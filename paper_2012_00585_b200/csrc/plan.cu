@@ -513,6 +513,92 @@ __global__ void k_pos_external(const int64_t* __restrict__ adj_ptr, const int32_
     }
 }
 
+// ---- external patterns: validation and CRAC -> CSR view on the device --------------------
+// (the reference trusts its own SparsityPattern; a caller's arrays are checked before any
+// indexing. Codes are ordered like the checks: the lowest failing one is reported.)
+enum ExtErr : unsigned {
+    kExtPtr0 = 1, kExtPtrMono, kExtCracEven, kExtCracPos, kExtCracPast, kExtCracEmpty, kExtColRange,
+    kExtColAsc, kExtOk = 0xffffffffu
+};
+
+const char* ext_err_text(unsigned c) {
+    switch (c) {
+        case kExtPtr0: return "row_ptr[0] must be 0";
+        case kExtPtrMono: return "row_ptr not monotone";
+        case kExtCracEven: return "CRAC row_ptr entries must be even";
+        case kExtCracPos: return "CRAC runs: value positions must start at 0 and increase";
+        case kExtCracPast: return "CRAC run extends past the last column";
+        case kExtCracEmpty: return "CRAC pattern without runs must have nnz 0";
+        case kExtColRange: return "pattern column outside the matrix";
+        case kExtColAsc: return "pattern columns not strictly ascending within a row";
+        default: return "malformed pattern";
+    }
+}
+
+__global__ void k_ext_check_ptr(const int64_t* __restrict__ ptr, int64_t n_rows, bool crac,
+                                unsigned* __restrict__ err) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= n_rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = ptr[r];
+        if (r == 0 && v != 0) atomicMin(err, (unsigned)kExtPtr0);
+        if (r < n_rows && v > ptr[r + 1]) atomicMin(err, (unsigned)kExtPtrMono);
+        if (crac && (v & 1)) atomicMin(err, (unsigned)kExtCracEven);
+    }
+}
+
+// build_crac_arrays layout (formats.cpp:21-41): pairs (column start, values position), closed by
+// (0, nnz). Every run's values position is the running count of the runs before it, so run
+// lengths (next position - this one) must be positive and the first position 0.
+__global__ void k_ext_check_runs(const int64_t* __restrict__ align, int64_t n_align, int64_t n_rows,
+                                 unsigned* __restrict__ err) {
+    const int64_t n_pairs = (n_align - 2) / 2;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_pairs;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t cs = align[2 * j], vs = align[2 * j + 1], ve = align[2 * j + 3];
+        if (cs < 0 || ve <= vs || (j == 0 && vs != 0)) atomicMin(err, (unsigned)kExtCracPos);
+        else if (cs + (ve - vs) > n_rows) atomicMin(err, (unsigned)kExtCracPast);
+    }
+    if (n_pairs == 0 && blockIdx.x == 0 && threadIdx.x == 0 && align[1] != 0)
+        atomicMin(err, (unsigned)kExtCracEmpty);
+}
+
+// CSR view of a (validated) CRAC pattern, for_each_in_row (formats.hpp:315-324): row r starts at
+// the values position of its first run (an empty row: of the next run).
+__global__ void k_ext_crac_csr_ptr(const int64_t* __restrict__ crac_ptr, const int64_t* __restrict__ align,
+                                   int64_t n_rows, int64_t* __restrict__ csr_ptr) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= n_rows;
+         r += (int64_t)gridDim.x * blockDim.x)
+        csr_ptr[r] = align[crac_ptr[r] + 1];
+}
+
+__global__ void k_ext_crac_cols(const int64_t* __restrict__ align, int64_t n_pairs, int64_t* __restrict__ cols) {
+    const int lane = threadIdx.x & 31;  // a warp per run
+    for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < n_pairs;
+         j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t cs = align[2 * j], vs = align[2 * j + 1], len = align[2 * j + 3] - vs;
+        for (int64_t k = lane; k < len; k += 32) cols[vs + k] = cs + k;
+    }
+}
+
+// Rows of the CSR view: columns inside the matrix and strictly ascending (a warp per row);
+// also the int32 column copy the plan keeps and the longest row.
+__global__ void k_ext_check_rows(const int64_t* __restrict__ ptr, const int64_t* __restrict__ cols,
+                                 int64_t n_rows, int32_t* __restrict__ ncol, unsigned* __restrict__ err,
+                                 unsigned long long* __restrict__ max_len) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n_rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t lo = ptr[r], hi = ptr[r + 1];
+        for (int64_t i = lo + lane; i < hi; i += 32) {
+            const int64_t c = cols[i];
+            if (c < 0 || c >= n_rows) atomicMin(err, (unsigned)kExtColRange);
+            else if (i > lo && cols[i - 1] >= c) atomicMin(err, (unsigned)kExtColAsc);
+            ncol[i] = static_cast<int32_t>(c);
+        }
+        if (lane == 0) atomicMax(max_len, static_cast<unsigned long long>(hi - lo));
+    }
+}
+
 // Colour-ordered incidences (FEA_DET_COLOUR as a segmented reduction): keys for a
 // two-pass LSD stable sort, first by colour, then by node — each node's incidences end up
 // in ascending (colour, element id).
@@ -1158,60 +1244,63 @@ fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, in
         DeviceScope ds(device);
         Stream st;
         cudaStream_t s = st.s;
-        // Host copies of the caller's pattern (reference arrays live on the host).
-        const bool dev_in = is_device_ptr(row_ptr);
-        std::vector<int64_t> h_ptr(static_cast<size_t>(n_rows + 1));
-        FEA_CK(cudaMemcpy(h_ptr.data(), row_ptr, h_ptr.size() * 8, cudaMemcpyDefault));
-        std::vector<int64_t> h_csr_ptr, h_cols, h_crac_ptr, h_align;
-        FEA_REQUIRE(h_ptr[0] == 0, FEA_ERR_INVALID, "row_ptr[0] must be 0");
-        for (int64_t r = 0; r < n_rows; ++r)
-            FEA_REQUIRE(h_ptr[r] <= h_ptr[r + 1], FEA_ERR_INVALID, "row_ptr not monotone");
-        FEA_REQUIRE(h_ptr[n_rows] <= (int64_t{1} << 40), FEA_ERR_INVALID, "row_ptr[n_rows] out of range");
-        if (format == FEA_FORMAT_CSR) {
-            h_csr_ptr = h_ptr;
-            h_cols.resize(static_cast<size_t>(h_ptr[n_rows]));
-            if (!h_cols.empty())
-                FEA_CK(cudaMemcpy(h_cols.data(), idx, h_cols.size() * 8, cudaMemcpyDefault));
+        // The caller's arrays (host, like the reference's, or device) are validated and turned
+        // into the plan's layout on the device: nothing here is O(nnz) on the host.
+        const bool crac = format == FEA_FORMAT_CRAC;
+        FEA_REQUIRE(!crac || idx, FEA_ERR_INVALID, "a CRAC pattern needs its col_align array (at least (0, 0))");
+        int64_t first = 0, last = 0;
+        FEA_CK(cudaMemcpy(&first, row_ptr, 8, cudaMemcpyDefault));
+        FEA_CK(cudaMemcpy(&last, row_ptr + n_rows, 8, cudaMemcpyDefault));
+        FEA_REQUIRE(first == 0, FEA_ERR_INVALID, "row_ptr[0] must be 0");
+        FEA_REQUIRE(last >= 0, FEA_ERR_INVALID, "row_ptr not monotone");
+        FEA_REQUIRE(last <= (int64_t{1} << 40), FEA_ERR_INVALID, "row_ptr[n_rows] out of range");
+        DevBuf hold_ptr, hold_idx, d_err, d_max;
+        auto on_device = [&](const int64_t* src, int64_t n, DevBuf& hold) -> const int64_t* {
+            if (n == 0 || is_device_ptr(src)) return src;
+            hold.alloc(static_cast<size_t>(n) * 8);
+            FEA_CK(cudaMemcpyAsync(hold.p, src, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice, s));
+            return hold.as<int64_t>();
+        };
+        const int64_t* in_ptr = on_device(row_ptr, n_rows + 1, hold_ptr);
+        d_err.alloc(4);
+        d_max.alloc(8);
+        FEA_CK(cudaMemsetAsync(d_err.p, 0xff, 4, s));
+        FEA_CK(cudaMemsetAsync(d_max.p, 0, 8, s));
+        auto check = [&] {
+            unsigned h = kExtOk;
+            FEA_CK(cudaGetLastError());
+            FEA_CK(cudaMemcpyAsync(&h, d_err.p, 4, cudaMemcpyDeviceToHost, s));
+            FEA_CK(cudaStreamSynchronize(s));
+            FEA_REQUIRE(h == kExtOk, FEA_ERR_INVALID, ext_err_text(h));
+        };
+        k_ext_check_ptr<<<grid_for(n_rows + 1, 256), 256, 0, s>>>(in_ptr, n_rows, crac, d_err.as<unsigned>());
+        check();  // the row pointers are safe to index with from here on
+        // CSR view: d_ptr / d_cols (the caller's own arrays for a CSR pattern)
+        DevBuf own_ptr, own_cols, miss;
+        const int64_t* d_ptr = in_ptr;
+        const int64_t* d_cols = nullptr;
+        const int64_t* d_cptr = nullptr;
+        const int64_t* d_align = nullptr;
+        int64_t nnz = last;
+        if (!crac) {
+            d_cols = on_device(idx, nnz, hold_idx);
         } else {
-            h_crac_ptr = h_ptr;
-            // build_crac_arrays layout (formats.cpp:21-41): row_ptr in col_align entry units, even,
-            // 2 * runs at the end; pairs (column start, values position) with the final (0, nnz)
-            for (int64_t r = 0; r <= n_rows; ++r)
-                FEA_REQUIRE((h_ptr[r] & 1) == 0, FEA_ERR_INVALID, "CRAC row_ptr entries must be even");
-            const int64_t n_align = h_ptr[n_rows] + 2;
-            h_align.resize(static_cast<size_t>(n_align));
-            FEA_CK(cudaMemcpy(h_align.data(), idx, h_align.size() * 8, cudaMemcpyDefault));
-            // every run's values position is the running count of the runs before it, and run
-            // lengths (next position - this one) are positive: the CSR view below then has
-            // exactly h_align[last + 1] entries in values order
-            for (int64_t i = 0; i + 2 < n_align; i += 2) {
-                FEA_REQUIRE(h_align[i] >= 0 && h_align[i + 3] > h_align[i + 1] && h_align[1] == 0,
-                            FEA_ERR_INVALID, "CRAC runs: value positions must start at 0 and increase");
-                FEA_REQUIRE(h_align[i] + (h_align[i + 3] - h_align[i + 1]) <= n_rows, FEA_ERR_INVALID,
-                            "CRAC run extends past the last column");
-            }
-            FEA_REQUIRE(n_align > 2 || h_align[1] == 0, FEA_ERR_INVALID, "CRAC pattern without runs must have nnz 0");
-            // CSR view of the CRAC pattern (for_each_in_row, formats.hpp:315-324)
-            h_csr_ptr.resize(static_cast<size_t>(n_rows + 1));
-            for (int64_t r = 0; r < n_rows; ++r) {
-                h_csr_ptr[r] = h_align[h_crac_ptr[r] + 1];
-                for (int64_t i = h_crac_ptr[r]; i < h_crac_ptr[r + 1]; i += 2) {
-                    const int64_t cs = h_align[i], vs = h_align[i + 1], ve = h_align[i + 3];
-                    for (int64_t k = 0; k < ve - vs; ++k) h_cols.push_back(cs + k);
-                }
-            }
-            h_csr_ptr[n_rows] = static_cast<int64_t>(h_cols.size());
-            if (n_rows > 0) h_csr_ptr[0] = 0;
-        }
-        (void)dev_in;
-        for (int64_t r = 0; r < n_rows; ++r) {
-            FEA_REQUIRE(h_csr_ptr[r] <= h_csr_ptr[r + 1], FEA_ERR_INVALID, "row_ptr not monotone");
-            for (int64_t i = h_csr_ptr[r]; i < h_csr_ptr[r + 1]; ++i) {
-                FEA_REQUIRE(h_cols[i] >= 0 && h_cols[i] < n_rows, FEA_ERR_INVALID,
-                            "pattern column outside the matrix");
-                FEA_REQUIRE(i == h_csr_ptr[r] || h_cols[i - 1] < h_cols[i], FEA_ERR_INVALID,
-                            "pattern columns not strictly ascending within a row");
-            }
+            const int64_t n_align = last + 2;
+            d_cptr = in_ptr;
+            d_align = on_device(idx, n_align, hold_idx);
+            k_ext_check_runs<<<grid_for(n_align / 2, 256), 256, 0, s>>>(d_align, n_align, n_rows,
+                                                                        d_err.as<unsigned>());
+            check();
+            FEA_CK(cudaMemcpy(&nnz, d_align + n_align - 1, 8, cudaMemcpyDefault));
+            FEA_REQUIRE(nnz >= 0 && nnz <= (int64_t{1} << 40), FEA_ERR_INVALID, "CRAC nnz out of range");
+            own_ptr.alloc((n_rows + 1) * 8);
+            own_cols.alloc(static_cast<size_t>(nnz) * 8);
+            k_ext_crac_csr_ptr<<<grid_for(n_rows + 1, 256), 256, 0, s>>>(d_cptr, d_align, n_rows,
+                                                                         own_ptr.as<int64_t>());
+            k_ext_crac_cols<<<grid_for((n_align - 2) / 2 * 32, 256), 256, 0, s>>>(d_align, (n_align - 2) / 2,
+                                                                                   own_cols.as<int64_t>());
+            d_ptr = own_ptr.as<int64_t>();
+            d_cols = own_cols.as<int64_t>();
         }
         auto p = std::make_unique<fea_plan>();
         p->device = device;
@@ -1222,40 +1311,25 @@ fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, in
         p->n_rows = n_rows;
         p->row_begin = 0;
         p->row_end = n_rows;
+        // node-level pattern == the caller's pattern (d = 1)
+        p->nptr.alloc((n_rows + 1) * 8);
+        FEA_CK(cudaMemcpyAsync(p->nptr.p, d_ptr, (n_rows + 1) * 8, cudaMemcpyDeviceToDevice, s));
+        p->ncol.alloc(static_cast<size_t>(nnz) * 4);
+        if (n_rows > 0)
+            k_ext_check_rows<<<grid_for(n_rows * 32, 256), 256, 0, s>>>(
+                d_ptr, d_cols, n_rows, p->ncol.as<int32_t>(), d_err.as<unsigned>(),
+                d_max.as<unsigned long long>());
+        check();
+        unsigned long long max_len = 0;
+        FEA_CK(cudaMemcpy(&max_len, d_max.p, 8, cudaMemcpyDeviceToHost));
+        FEA_REQUIRE(max_len <= 65536, FEA_ERR_INVALID, "pattern row longer than 65536 entries");
         build_elements(p.get(), elem_dofs, 1, s);
         build_adjacency(p.get(), s);
-        // node-level pattern == the caller's pattern (d = 1)
-        const int64_t nnz = h_csr_ptr[n_rows];
-        p->nptr.alloc((n_rows + 1) * 8);
-        FEA_CK(cudaMemcpyAsync(p->nptr.p, h_csr_ptr.data(), (n_rows + 1) * 8,
-                               cudaMemcpyHostToDevice, s));
-        std::vector<int32_t> h_cols32(h_cols.begin(), h_cols.end());
-        p->ncol.alloc(nnz * 4);
-        if (nnz > 0)
-            FEA_CK(cudaMemcpyAsync(p->ncol.p, h_cols32.data(), nnz * 4, cudaMemcpyHostToDevice, s));
-        int64_t max_len = 0;
-        for (int64_t r = 0; r < n_rows; ++r) max_len = std::max(max_len, h_csr_ptr[r + 1] - h_csr_ptr[r]);
-        FEA_REQUIRE(max_len <= 65536, FEA_ERR_INVALID, "pattern row longer than 65536 entries");
         p->max_cnt = static_cast<int32_t>(max_len);
         p->pos_bytes = max_len <= 256 ? 1 : 2;
         p->pstride = ((p->npe * p->pos_bytes + 3) / 4 * 4) / p->pos_bytes;
         p->nnz_nodes = nnz;
         p->nnz = nnz;
-        // device copies for the lookup kernel
-        DevBuf d_ptr, d_cols, d_cptr, d_align, miss;
-        d_ptr.alloc((n_rows + 1) * 8);
-        FEA_CK(cudaMemcpyAsync(d_ptr.p, h_csr_ptr.data(), (n_rows + 1) * 8, cudaMemcpyHostToDevice, s));
-        d_cols.alloc(nnz * 8);
-        if (nnz > 0)
-            FEA_CK(cudaMemcpyAsync(d_cols.p, h_cols.data(), nnz * 8, cudaMemcpyHostToDevice, s));
-        if (format == FEA_FORMAT_CRAC) {
-            d_cptr.alloc((n_rows + 1) * 8);
-            d_align.alloc(h_align.size() * 8);
-            FEA_CK(cudaMemcpyAsync(d_cptr.p, h_crac_ptr.data(), (n_rows + 1) * 8,
-                                   cudaMemcpyHostToDevice, s));
-            FEA_CK(cudaMemcpyAsync(d_align.p, h_align.data(), h_align.size() * 8,
-                                   cudaMemcpyHostToDevice, s));
-        }
         miss.alloc(8);
         FEA_CK(cudaMemsetAsync(miss.p, 0xff, 8, s));
         p->posA.alloc(p->n_adj * p->pstride * p->pos_bytes + 64);
@@ -1265,9 +1339,7 @@ fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, in
 #define FEA_LAUNCH_EXT(T, C)                                                                   \
     k_pos_external<T, C><<<blocks, 256, 0, s>>>(                                               \
         p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe, n_rows, \
-        d_ptr.as<int64_t>(), d_cols.as<int64_t>(), d_cptr.as<int64_t>(), d_align.as<int64_t>(), \
-        p->pstride, p->posA.as<T>(), miss.as<unsigned long long>())
-            const bool crac = format == FEA_FORMAT_CRAC;
+        d_ptr, d_cols, d_cptr, d_align, p->pstride, p->posA.as<T>(), miss.as<unsigned long long>())
             if (p->pos_bytes == 1) {
                 if (crac) FEA_LAUNCH_EXT(uint8_t, true); else FEA_LAUNCH_EXT(uint8_t, false);
             } else {

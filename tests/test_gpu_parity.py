@@ -139,8 +139,9 @@ def test_accumulate_is_left_fold_from_existing(gpu, orc, mesh, n, d, perm):
         assert v.cpu().numpy().tobytes() == want.tobytes()
 
 
+@pytest.mark.parametrize("where", ["host", "device"])
 @pytest.mark.parametrize("fmt", ["csr", "crac"])
-def test_external_pattern_superset(gpu, orc, fmt):
+def test_external_pattern_superset(gpu, orc, fmt, where):
     """A caller's pattern with extra entries (random_pattern-style superset): slots resolved
     by the device CSR search / CRAC Listing-1 search; values bit-exact vs sequential."""
     import torch
@@ -157,13 +158,16 @@ def test_external_pattern_superset(gpu, orc, fmt):
     S = orc.Pattern.from_arrays(srp, scs)
     Kh = orc.fill_k(1, conn.shape[0], ed.shape[1])
     want = S.assemble_sequential(ed, Kh)
+    put = (lambda a: torch.from_numpy(a).cuda()) if where == "device" else (lambda a: a)
     if fmt == "csr":
-        plan = gpu.Plan.with_pattern(ed, n_rows, srp, scs, "csr")
+        plan = gpu.Plan.with_pattern(ed, n_rows, put(srp), put(scs), "csr")
     else:
         cp, ca = S.crac()
-        plan = gpu.Plan.with_pattern(ed, n_rows, cp, ca, "crac")
+        plan = gpu.Plan.with_pattern(ed, n_rows, put(cp), put(ca), "crac")
     with plan:
         assert plan.nnz == S.nnz and plan.missing_entry() is None
+        prp, pcs = plan.csr()  # the plan's view of the caller's pattern (CRAC: expanded on the device)
+        assert np.array_equal(prp, srp) and np.array_equal(pcs, scs)
         got = plan.assemble(torch.from_numpy(Kh).cuda(), strategy="sorted").cpu().numpy()
         assert got.tobytes() == want.tobytes()
         got_a = plan.assemble(torch.from_numpy(Kh).cuda(), strategy="atomic").cpu().numpy()
@@ -186,6 +190,9 @@ def test_external_pattern_malformed_is_invalid(gpu, orc):
     a = ca.copy(); a[3] = a[5] + 2; bad.append((cp, a, "crac"))
     a = ca.copy(); a[-1] = a[-3]; bad.append((cp, a, "crac"))
     a = ca.copy(); a[-4] = n_rows; bad.append((cp, a, "crac"))
+    c = cs.copy(); c[rp[2]], c[rp[2] + 1] = c[rp[2] + 1], c[rp[2]]; bad.append((rp, c, "csr"))  # not ascending
+    c = cs.copy(); c[0] = -1; bad.append((rp, c, "csr"))
+    r = rp.copy(); r[-1] = -5; bad.append((r, cs, "csr"))
     for r, c, fmt in bad:
         with pytest.raises(ValueError):
             gpu.Plan.with_pattern(ed, n_rows, r, c, fmt)
