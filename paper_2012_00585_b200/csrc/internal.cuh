@@ -56,13 +56,15 @@ struct DeviceScope {
     ~DeviceScope();
 };
 
-// Environment A/B switches of the numeric kernels, read once per process
-// instead of on every assembly.
+// Environment A/B switches of the numeric kernels, read once per plan (at
+// creation) instead of on every assembly.
 struct Knobs {
     bool atomic_legacy, atomic_no_patch, slot_no_fixed, cn_unpacked, cn_no_records, d1_no_direct, d1_no_vec;
+    bool d1_no_lane;  // FEA_D1_NO_LANE: shared-memory fold (k_gather_d1g) instead of lane-owned slots
+    bool d1_rec8;  // FEA_D1_REC8: 8-byte lane records even where the compact 4-byte form fits
     int d1_acc_mod, d1v_acc_mod;  // accumulator stride residues (mod 16 doubles)
 };
-const Knobs& knobs();
+Knobs read_knobs();
 
 // Stream/event set of the end-to-end host paths (fea_assemble_host pipeline and
 // fea_assemble_host_batch), created on first use and kept with the plan.
@@ -145,6 +147,21 @@ struct fea_plan {
     feagpu::DevBuf trav_meta;  // int64 [n_own] values start << 20 | row length
     feagpu::DevBuf trav_rec;   // int32 [n_adj*trav_rw] {entry, position words[, pad]}
     feagpu::DevBuf trav_recC;  // the same for the colour-ordered incidences (adjC / posAC)
+    // d = 1, npe = 4, rows of <= 16 nodes: lane-owned slots (k_gather_d1r). Every slot of a node's
+    // row belongs to one of the 4 lanes of its group (a proper 4-colouring of the node's star:
+    // the 4 nodes of each incident element get 4 distinct lanes) and to one of that lane's
+    // registers, so the fold needs no shared memory and no warp synchronisation.
+    feagpu::DevBuf ln_slot;    // uint8 [n_own*16] lane | accumulator << 2 per (traversal position, slot)
+    // int4 [2*n_own] per traversal position: {values start << 20 | the diagonal slot << 16 |
+    // accumulators used per lane (4 x 4 bits) (int64), first record | record count << 40 (int64)},
+    // {4 * lowest K row, lanes 1..3: the slots of their accumulators, 4 bits each}
+    feagpu::DevBuf ln_hdr;
+    feagpu::DevBuf ln_rec;     // records, sorted incidences: uint32 (compact) or int2 {entry, lane word}
+    feagpu::DevBuf ln_recC;    // the same for the colour-ordered incidences
+    bool ln_ok = false;
+    bool ln_rec4 = false;      // compact 4-byte records (entry offset fits next to the lane fields)
+    int32_t ln_q = 0;          // most accumulators any lane needs
+    int32_t ln_wq[3] = {0, 0, 0};  // record bits of the accumulator field of lanes 1..3
     feagpu::DevBuf cnr_hdr;    // int4 [n_own]: values start (int64), row length | n << 16, accumulator offset
     feagpu::DevBuf cnr_rec;    // [n_own][8][32 B]: {entry, npe position bytes} per incidence (k_gather_cnr)
     feagpu::DevBuf cnr_recC;   // the same for the colour-ordered incidences (reset by set_colouring)
@@ -160,6 +177,7 @@ struct fea_plan {
     // external-pattern missing entry (lowest element)
     int64_t miss_e = -1, miss_r = -1, miss_c = -1;
     // bookkeeping
+    feagpu::Knobs kn = {};     // A/B switches as the environment had them when the plan was created
     int32_t last_launches = 0;
     bool gen_on = false;       // fea_assemble_seeded in progress: kernels generate K
     uint64_t gen_seed = 0;

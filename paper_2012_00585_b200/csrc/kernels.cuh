@@ -1098,6 +1098,109 @@ __global__ void __launch_bounds__(kWarps * 32, FEA_D1G_MINB)
     for (int i = gl; i < rl; i += G) __stcs(values + vb + i, acc[i]);
 }
 
+// Lane-owned slots (npe = 4, d = 1, rows of <= 16 nodes, traversal records; materialized K).
+// k_gather_d1g folds into a shared-memory accumulator at data-dependent slots: a bank-conflicted
+// read-add-write per entry plus a warp barrier per incidence, and its 8-byte records cost 0.4 GB
+// on cfg3. Here the plan has given every slot of the node's row to one lane of the node's
+// group and one of that lane's accumulators (fea_plan::ln_*: lane 0 = the diagonal slot,
+// lanes 1..3 = a 3-colouring of the node's link, so the 4 columns of every incident element
+// fall on 4 distinct lanes), and every record tells lane c which column of the incidence's K
+// row is its own and which accumulator it goes to: per incidence a lane does one 8-byte K load
+// (the 4 lanes read the 4 doubles of one 32 B sector, as before) and one add into an
+// accumulator no other lane touches - no warp synchronisation, no bank conflicts. Each slot
+// still folds its contributions in record order from the start value: same bits.
+// k_gather_d1s: 64 nodes per CTA, the lane's accumulators acc[q][thread] in shared memory, so
+// the kernel fits 32 registers and 64 warps per SM. The bare access pattern (records -> K rows
+// -> values, tools/gather_probe_d1.py) needs that residency: its dependent round trips per node
+// are covered by nodes in flight, not by loads in flight per lane (U = 2..8, a record prefetch
+// a batch ahead and every store cache policy measured within 2 %). Measured on cfg3 and
+// dropped: register accumulators with one predicated add per register (66 registers, 28
+// warps/SM: 0.626 ms; as plain C++ the compiler turns the register select into a jump table,
+// 0.98 ms) and a persistent CTA whose node headers and records arrive by TMA bulk copies two
+// tiles ahead with two K batches in flight per lane (56 registers: 0.92 ms, DRAM reads 2.67
+// GB - the static tile stride lets CTAs drift apart and the K lines shared by neighbouring
+// nodes leave L2), against 0.547 ms for this form with 8-byte records.
+// Record word (LSB first): for lanes 1, 2, 3 in turn the element column the lane loads (2 bits)
+// and its accumulator (wq1, wq2, wq3 bits, plan-wide widths), then - compact 4-byte records,
+// used when it fits - the entry minus 4 * the node's lowest K row; 8-byte records keep the
+// entry in a word of its own. Lane 0 owns only the node's diagonal slot: its column is
+// entry & 3 (the bits right above the lane fields), its accumulator 0.
+#ifndef FEA_D1S_U
+#define FEA_D1S_U 4  // records + K rows in flight per lane (cfg3: 2, 4, 6, 8 within 2 %)
+#endif
+#ifndef FEA_D1S_MINB
+#define FEA_D1S_MINB 8
+#endif
+constexpr int kD1sThreads = 256;
+template <int U, bool REC4>
+__global__ void __launch_bounds__(kD1sThreads, FEA_D1S_MINB)
+    k_gather_d1s(const double* __restrict__ K, int64_t n_own, int accumulate, const int4* __restrict__ hdr,
+                 const void* __restrict__ lrec, int q_max, int wq1, int wq2, int wq3,
+                 double* __restrict__ values) {
+    extern __shared__ double sacc[];
+    constexpr int T = kD1sThreads;
+    using Rec = typename std::conditional<REC4, uint32_t, int2>::type;
+    const int gl = threadIdx.x & 3;
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * (T / 4) + (threadIdx.x >> 2);
+    int64_t vb = 0, a0 = 0;
+    int n = 0, nq = 0;
+    uint32_t lw = 0, base = 0;
+    if (t < n_own) {  // plan metadata: may run ahead of the previous kernel's end (PDL)
+        const int4 h0 = __ldg(hdr + 2 * t), h1 = __ldg(hdr + 2 * t + 1);
+        const int64_t li = (static_cast<int64_t>(h0.y) << 32) | static_cast<uint32_t>(h0.x);
+        const int64_t an = (static_cast<int64_t>(h0.w) << 32) | static_cast<uint32_t>(h0.z);
+        vb = li >> 20;
+        nq = static_cast<int>(li >> (4 * gl)) & 15;
+        a0 = an & ((int64_t{1} << 40) - 1);
+        n = static_cast<int>(an >> 40);
+        base = static_cast<uint32_t>(h1.x);
+        lw = gl == 0 ? (static_cast<uint32_t>(li >> 16) & 15u)
+                     : static_cast<uint32_t>(gl == 1 ? h1.y : gl == 2 ? h1.z : h1.w);
+    }
+    const int n_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(n)));
+    const Rec* src = static_cast<const Rec*>(lrec) + a0;
+    double* acc = sacc + threadIdx.x;
+    // the lane's field of a record word: column at off, accumulator above it (mask mq)
+    const int sh_e = 6 + wq1 + wq2 + wq3;
+    const int off = gl == 0 ? sh_e : gl == 1 ? 0 : gl == 2 ? 2 + wq1 : 4 + wq1 + wq2;
+    const uint32_t mq = gl == 0 ? 0u : (1u << (gl == 1 ? wq1 : gl == 2 ? wq2 : wq3)) - 1u;
+    pdl_wait();  // K and values only after the previous kernel of the stream has finished
+    pdl_launch_dependents();
+    for (int q = 0; q < q_max; ++q)
+        acc[q * T] = (accumulate && q < nq) ? values[vb + ((lw >> (4 * q)) & 15u)] : 0.0;
+    for (int k0 = 0; k0 < n_max; k0 += U) {
+        Rec r[U];
+        double kv[U];
+        int qv[U];
+        // (ternaries, not branches: the loads stay predicated and issue back to back)
+#pragma unroll
+        for (int u = 0; u < U; ++u) r[u] = k0 + u < n ? __ldg(src + k0 + u) : Rec{};
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            uint32_t w, ent;
+            if constexpr (REC4) {
+                w = r[u];
+                ent = base + (w >> sh_e);
+            } else {
+                w = static_cast<uint32_t>(r[u].y);
+                ent = static_cast<uint32_t>(r[u].x);
+            }
+            // lane 0: off points at the entry's low bits (8-byte records: taken from ent)
+            const uint32_t f = (REC4 || gl != 0) ? w >> off : ent;
+            kv[u] = k0 + u < n ? kload_d1(K + static_cast<int64_t>(ent) * 4 + (f & 3u)) : 0.0;
+            qv[u] = static_cast<int>((f >> 2) & mq);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (k0 + u < n) {
+                FEA_DCHECK(qv[u] < nq);
+                acc[qv[u] * T] += kv[u];
+            }
+    }
+    for (int q = 0; q < q_max; ++q)
+        if (q < nq) __stcs(values + vb + ((lw >> (4 * q)) & 15u), acc[q * T]);
+}
+
 // ---------------------------------------------------------------------------
 // Deterministic owner-computes gather, lane = slot (d in {2,3,4}, npe <= 8, rows <= 32 nodes)
 // ---------------------------------------------------------------------------
@@ -2156,7 +2259,7 @@ void run_gather_slot(fea_plan* p, const Incidences& in, const double* K, double*
     const bool sorted_inc = in.adj == p->adj.as<int32_t>();
     feagpu::DevBuf& fx = sorted_inc ? p->slot_rec : p->slot_recC;
     const bool fixed = !p->gen_on && (sorted_inc || in.adj == p->adjC.as<int32_t>()) &&
-                       !knobs().slot_no_fixed && (fx.p || !capturing(s));
+                       !p->kn.slot_no_fixed && (fx.p || !capturing(s));
     if (fixed && !fx.p) {
         if (!p->slot_hdr.p) p->slot_hdr.alloc(std::max<int64_t>(p->n_own, 1) * 16);
         fx.alloc(std::max<int64_t>(p->n_own, 1) * nbuf * 16);
@@ -2223,7 +2326,7 @@ __global__ void k_cta_acc_max(const int32_t* __restrict__ order, const int64_t* 
 }
 
 int64_t cn_cta_acc(fea_plan* p, int per_cta, cudaStream_t s) {
-    if (knobs().cn_unpacked) return static_cast<int64_t>(per_cta) * (p->d * p->d * p->max_cnt + 1);
+    if (p->kn.cn_unpacked) return static_cast<int64_t>(per_cta) * (p->d * p->d * p->max_cnt + 1);
     if (p->cn_cta_acc > 0 && p->cn_cta_per == per_cta) return p->cn_cta_acc;
     DevBuf out;
     out.alloc(8);
@@ -2254,7 +2357,7 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
     if (G == 32 && sizeof(PosT) == 1 && !p->dup_nodes && p->max_adj <= kCnrSlots &&
         p->npe <= kCnrBytes - 4 && (in.adj == p->adj.as<int32_t>() || in.adj == p->adjC.as<int32_t>()) &&
-        !knobs().cn_no_records &&
+        !p->kn.cn_no_records &&
         ((p->cnr_hdr.p && (in.adj == p->adj.as<int32_t>() ? p->cnr_rec.p : p->cnr_recC.p)) || !capturing(s))) {
         // built lazily on the first assembly of each incidence order: 16 + 256 bytes per node
         feagpu::DevBuf& recs = in.adj == p->adj.as<int32_t>() ? p->cnr_rec : p->cnr_recC;
@@ -2314,7 +2417,7 @@ void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* v
     // (0.642 ms vs 0.664 at 15 and 0.670 at 1)
     int acc_stride = std::max(p->max_cnt, 1);
     int acc_mod = 3;
-    if (knobs().d1_acc_mod >= 0) acc_mod = knobs().d1_acc_mod;
+    if (p->kn.d1_acc_mod >= 0) acc_mod = p->kn.d1_acc_mod;
     while ((acc_stride & 15) != acc_mod) ++acc_stride;
     const int cap = static_cast<int>(std::max<int64_t>(p->max_adj, 1));
     const int pw = p->pstride * static_cast<int>(sizeof(PosT)) / 4;
@@ -2335,10 +2438,35 @@ void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* v
     const DevBuf& recs = in.adj == p->adj.as<int32_t>() ? p->trav_rec : p->trav_recC;
     const bool trav = recs.p != nullptr && (in.adj == p->adj.as<int32_t>() || in.adj == p->adjC.as<int32_t>());
     FEA_REQUIRE(!trav || p->trav_rw == rw, FEA_ERR_INVALID, "traversal record width mismatch");
+    // lane-owned slots (the plan coloured every node's star with 4 lanes)
+    if (G == 4 && p->npe == 4 && trav && rw == 2 && !p->dup_nodes && sizeof(PosT) == 1 && !p->gen_on &&
+        p->ln_ok && !p->kn.d1_no_lane) {
+        const DevBuf& lrecs = in.adj == p->adj.as<int32_t>() ? p->ln_rec : p->ln_recC;
+        FEA_REQUIRE(lrecs.p != nullptr, FEA_ERR_INVALID, "lane records missing");
+        const Win wn = window_of(p);
+        {
+            void (*ks)(const double*, int64_t, int, const int4*, const void*, int, int, int, int, double*) =
+                p->ln_rec4 ? k_gather_d1s<FEA_D1S_U, true> : k_gather_d1s<FEA_D1S_U, false>;
+            const size_t smems = static_cast<size_t>(p->ln_q) * kD1sThreads * sizeof(double);
+            launch_prep(p, ks, kD1sThreads, smems);
+            if (p->win_query) {
+                p->win_ok = true;
+                return;
+            }
+            const int64_t blocks_s = (wn.n + kD1sThreads / 4 - 1) / (kD1sThreads / 4);
+            if (blocks_s == 0) return;
+            launch_pdl(ks, static_cast<unsigned>(blocks_s), kD1sThreads, smems, s, K, wn.n, accumulate ? 1 : 0,
+                       p->ln_hdr.as<int4>() + 2 * wn.t0, static_cast<const void*>(lrecs.p), p->ln_q, p->ln_wq[0],
+                       p->ln_wq[1], p->ln_wq[2], values);
+            FEA_CK(cudaGetLastError());
+            p->last_launches += 1;
+            return;
+        }
+    }
     // npe = 4 with traversal records: direct-record kernel for a materialized K, two-lane
     // kernel for the fused supplier
     if (G == 4 && p->npe == 4 && trav && rw == 2 && !p->dup_nodes && sizeof(PosT) == 1 && !p->gen_on &&
-        !knobs().d1_no_direct) {
+        !p->kn.d1_no_direct) {
         const size_t smemg = static_cast<size_t>(kWarps) * GPW * acc_stride * sizeof(double);
         auto kg = k_gather_d1g<FEA_D1G_U>;
         launch_prep(p, kg, kWarps * 32, smemg);
@@ -2357,11 +2485,11 @@ void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* v
         return;
     }
     if (G == 4 && p->npe == 4 && trav && rw == 2 && !p->dup_nodes && sizeof(PosT) == 1 && p->gen_on &&
-        !knobs().d1_no_vec) {
+        !p->kn.d1_no_vec) {
         constexpr int GPW2 = 16;
         int acc_stride2 = std::max(p->max_cnt, 1);
         int acc_mod2 = 3;
-        if (knobs().d1v_acc_mod >= 0) acc_mod2 = knobs().d1v_acc_mod;
+        if (p->kn.d1v_acc_mod >= 0) acc_mod2 = p->kn.d1v_acc_mod;
         while ((acc_stride2 & 15) != acc_mod2) ++acc_stride2;
         const size_t smem2 = static_cast<size_t>(kWarps) * GPW2 *
                              (acc_stride2 * sizeof(double) + static_cast<size_t>(rec_stride) * sizeof(int32_t));

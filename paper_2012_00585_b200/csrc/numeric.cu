@@ -87,8 +87,8 @@ void ensure_element_maps(fea_plan* p, cudaStream_t s) {
 // distinct (owned row node, column node) pairs, sorted by (row, position), and per element the
 // pair index of each (a, b). Host work, once per plan (on the first atomic assembly).
 void build_patches(fea_plan* p, cudaStream_t s) {
-    if (p->npe != 8 || p->d > 3 || p->pos_bytes != 1 || p->dup_nodes || p->E == 0 || knobs().atomic_no_patch ||
-        knobs().atomic_legacy || p->pk_n > 0)
+    if (p->npe != 8 || p->d > 3 || p->pos_bytes != 1 || p->dup_nodes || p->E == 0 || p->kn.atomic_no_patch ||
+        p->kn.atomic_legacy || p->pk_n > 0)
         return;
     constexpr int NPE = 8, NN = 64, P = kPatchElems;
     const int64_t E = p->E;
@@ -270,7 +270,7 @@ void build_patches(fea_plan* p, cudaStream_t s) {
 void build_atomic_maps(fea_plan* p, cudaStream_t s) {
     const bool shape = (p->d >= 1 && p->d <= 3 && (p->npe == 4 || p->npe == 8)) ||
                        ((p->d == 1 || p->d == 3) && p->npe == 27);  // k_atomic_staged / k_atomic_cta
-    if (!shape || p->E == 0 || knobs().atomic_legacy ||
+    if (!shape || p->E == 0 || p->kn.atomic_legacy ||
         static_cast<int64_t>(p->d) * p->max_cnt >= (1 << 20))
         return;
     const int mm = p->m * p->m;

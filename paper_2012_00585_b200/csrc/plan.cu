@@ -61,18 +61,16 @@ DeviceScope::~DeviceScope() {
     if (prev >= 0 && cur != prev) cudaSetDevice(prev);
 }
 
-const Knobs& knobs() {
-    static const Knobs k = [] {
-        auto on = [](const char* n) { return std::getenv(n) != nullptr; };
-        auto mod = [](const char* n) {
-            const char* e = std::getenv(n);
-            return e ? (std::atoi(e) & 15) : -1;
-        };
-        return Knobs{on("FEA_ATOMIC_LEGACY"), on("FEA_ATOMIC_NO_PATCH"), on("FEA_SLOT_NO_FIXED"), on("FEA_CN_UNPACKED"),
-                     on("FEA_CN_NO_RECORDS"), on("FEA_D1_NO_DIRECT"),    on("FEA_D1_NO_VEC"),
-                     mod("FEA_D1_ACC_STRIDE_MOD16"), mod("FEA_D1V_ACC_STRIDE_MOD16")};
-    }();
-    return k;
+Knobs read_knobs() {
+    auto on = [](const char* n) { return std::getenv(n) != nullptr; };
+    auto mod = [](const char* n) {
+        const char* e = std::getenv(n);
+        return e ? (std::atoi(e) & 15) : -1;
+    };
+    return Knobs{on("FEA_ATOMIC_LEGACY"), on("FEA_ATOMIC_NO_PATCH"), on("FEA_SLOT_NO_FIXED"), on("FEA_CN_UNPACKED"),
+                 on("FEA_CN_NO_RECORDS"), on("FEA_D1_NO_DIRECT"),    on("FEA_D1_NO_VEC"),
+                 on("FEA_D1_NO_LANE"),    on("FEA_D1_REC8"),
+                 mod("FEA_D1_ACC_STRIDE_MOD16"), mod("FEA_D1V_ACC_STRIDE_MOD16")};
 }
 
 void HostPipe::ensure_events(int n) {
@@ -871,6 +869,8 @@ __global__ void k_trav_records(const int32_t* __restrict__ order, const int64_t*
     }
 }
 
+void build_lane_slots(fea_plan* p, cudaStream_t s);
+
 // d = 1 sorted gather with a traversal order: incidence records in traversal order
 void build_traversal(fea_plan* p, cudaStream_t s) {
     p->trav_ptr.reset();
@@ -898,7 +898,221 @@ void build_traversal(fea_plan* p, cudaStream_t s) {
         p->trav_rec.as<int32_t>());
     FEA_CK(cudaGetLastError());
     p->trav_rw = rw;
+    build_lane_slots(p, s);
     FEA_CK(cudaStreamSynchronize(s));
+}
+
+// --- lane-owned slots (k_gather_d1s: d = 1, npe = 4, rows of <= 16 nodes) ---------------------
+// One thread per traversal position gives every slot of its node's row to one of the 4 lanes of
+// the node's group so that the 4 columns of every incident element fall on 4 distinct lanes.
+// The node's own (diagonal) slot shares an element with every other slot that any element
+// touches, so it takes lane 0 alone; the rest is a 3-colouring of the node's link (DSATUR: on a
+// Kuhn tet mesh the link is a triangulated sphere and every step after the first triangle is
+// forced). The three classes are renamed by size (smallest = lane 1), slots of one lane take
+// that lane's accumulators in slot order. A node that cannot be coloured, or needs more than 8
+// accumulators on one lane, sets the plan's fail flag and the shared-memory fold stays in use.
+// stats: [0] fail, [1..3] most accumulators on lane 1..3, [4] most on any lane,
+// [5] largest entry - 4 * lowest K row of the node (width of the compact record's entry field)
+__global__ void k_lane_colour(const int64_t* __restrict__ tptr, const int64_t* __restrict__ tmeta,
+                              const int2* __restrict__ trec, int64_t n_own, uint8_t* __restrict__ slotmap,
+                              int4* __restrict__ hdr, int* __restrict__ stats) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_own;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a0 = tptr[t];
+        const int n = static_cast<int>(tptr[t + 1] - a0);
+        const int64_t mt = tmeta[t];
+        const int rl = static_cast<int>(mt & 0xfffff);
+        if (rl > 16) {
+            atomicOr(stats, 1);
+            continue;
+        }
+        uint32_t adjm[16];
+        uint8_t used[16], col[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) adjm[i] = 0, used[i] = 0, col[i] = 0xff;
+        bool bad = false;
+        int diag = -1;
+        uint32_t emin = 0xffffffffu, emax = 0;
+        for (int k = 0; k < n; ++k) {
+            const int2 r = trec[a0 + k];
+            const uint32_t w = static_cast<uint32_t>(r.y);
+            uint32_t m = 0;
+            for (int b = 0; b < 4; ++b) {
+                const uint32_t sl = (w >> (8 * b)) & 0xffu;
+                if (sl >= static_cast<uint32_t>(rl)) bad = true;
+                m |= 1u << (sl & 15);
+            }
+            if (__popc(m) != 4) bad = true;
+            for (int b = 0; b < 4; ++b) adjm[(w >> (8 * b)) & 15] |= m;
+            const int dg = static_cast<int>((w >> (8 * (r.x & 3))) & 15u);  // the node's own column
+            if (diag >= 0 && dg != diag) bad = true;
+            diag = dg;
+            emin = min(emin, static_cast<uint32_t>(r.x));
+            emax = max(emax, static_cast<uint32_t>(r.x));
+        }
+        int cnt[4] = {0, 0, 0, 0};
+        if (diag >= 0 && !bad) {
+            col[diag] = 0;
+            cnt[0] = 1;
+            uint32_t nb = adjm[diag] & ~(1u << diag);
+            while (nb) {
+                const int u = __ffs(nb) - 1;
+                nb &= nb - 1;
+                used[u] |= 1;
+            }
+        }
+        for (int it = cnt[0]; it < rl && !bad; ++it) {
+            int best = -1, bkey = -1;
+            for (int sl = 0; sl < rl; ++sl) {
+                if (col[sl] != 0xff) continue;
+                const int key = __popc(used[sl]) * 64 + __popc(adjm[sl]);
+                if (key > bkey) bkey = key, best = sl;
+            }
+            int c = -1;
+            for (int q = 1; q < 4; ++q)
+                if (!((used[best] >> q) & 1) && (c < 0 || cnt[q] < cnt[c])) c = q;
+            if (c < 0) {
+                bad = true;
+                break;
+            }
+            col[best] = static_cast<uint8_t>(c);
+            ++cnt[c];
+            uint32_t nb = adjm[best] & ~(1u << best);
+            while (nb) {
+                const int u = __ffs(nb) - 1;
+                nb &= nb - 1;
+                used[u] |= static_cast<uint8_t>(1u << c);
+            }
+        }
+        if (bad || cnt[1] > 8 || cnt[2] > 8 || cnt[3] > 8) {
+            atomicOr(stats, 1);
+            continue;
+        }
+        // rename classes 1..3 by size (ties by class number): ren[old] = new lane
+        int ren[4] = {0, 1, 2, 3};
+        for (int i = 1; i < 4; ++i) {
+            int rank = 1;
+            for (int j = 1; j < 4; ++j)
+                if (j != i && (cnt[j] < cnt[i] || (cnt[j] == cnt[i] && j < i))) ++rank;
+            ren[i] = rank;
+        }
+        uint32_t lw[4] = {0, 0, 0, 0};
+        int nq[4] = {0, 0, 0, 0};
+        for (int sl = 0; sl < 16; ++sl) {
+            uint8_t cq = 0;
+            if (sl < rl) {
+                const int c = ren[col[sl]], q = nq[c]++;
+                lw[c] |= static_cast<uint32_t>(sl) << (4 * q);
+                cq = static_cast<uint8_t>(c | (q << 2));
+            }
+            slotmap[t * 16 + sl] = cq;
+        }
+        atomicMax(stats + 1, nq[1]);
+        atomicMax(stats + 2, nq[2]);
+        atomicMax(stats + 3, nq[3]);
+        atomicMax(stats + 4, max(max(nq[0], nq[1]), max(nq[2], nq[3])));
+        const uint32_t base = n > 0 ? (emin & ~3u) : 0u;
+        if (n > 0) atomicMax(stats + 5, static_cast<int>(min(emax - base, 0x7fffffffu)));
+        const int64_t li = ((mt >> 20) << 20) | nq[0] | (nq[1] << 4) | (nq[2] << 8) | (nq[3] << 12) |
+                           (static_cast<int64_t>(lw[0] & 15u) << 16);
+        const int64_t an = a0 | (static_cast<int64_t>(n) << 40);
+        hdr[2 * t] = make_int4(static_cast<int>(li & 0xffffffff), static_cast<int>(li >> 32),
+                               static_cast<int>(an & 0xffffffff), static_cast<int>(an >> 32));
+        hdr[2 * t + 1] = make_int4(static_cast<int>(base), static_cast<int>(lw[1]), static_cast<int>(lw[2]),
+                                   static_cast<int>(lw[3]));
+    }
+}
+
+// Records of the lane-owned gather from the traversal records {entry, position bytes}. Word
+// layout (LSB first): for lanes 1, 2, 3 in turn the element column the lane loads (2 bits) and
+// its accumulator (wq[c-1] bits, plan-wide widths), then - compact 4-byte form only - entry -
+// 4 * the node's lowest K row. Lane 0 takes the node's own column (entry & 3) and accumulator
+// 0. The 8-byte form keeps the entry in its own word.
+struct LaneFmt {
+    int wq[3];
+    int sh_e;  // 6 + wq[0] + wq[1] + wq[2]: first bit of the entry offset
+};
+template <bool REC4>
+__global__ void k_lane_records(const int64_t* __restrict__ tptr, const int2* __restrict__ trec,
+                               const uint8_t* __restrict__ slotmap, const int4* __restrict__ hdr, int64_t n_own,
+                               LaneFmt f, void* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n_own;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t a0 = tptr[t], n = tptr[t + 1] - a0;
+        const uint32_t base = static_cast<uint32_t>(hdr[2 * t + 1].x);
+        for (int64_t k = lane; k < n; k += 32) {
+            const int2 r = trec[a0 + k];
+            uint32_t word = 0;
+            for (int b = 0; b < 4; ++b) {
+                const uint32_t sl = (static_cast<uint32_t>(r.y) >> (8 * b)) & 15u;
+                const uint32_t cq = slotmap[t * 16 + sl];
+                const int c = static_cast<int>(cq & 3u);
+                if (c == 0) continue;  // the node's own column: b = entry & 3, accumulator 0
+                int off = 0;
+                for (int j = 0; j < c - 1; ++j) off += 2 + f.wq[j];
+                word |= (static_cast<uint32_t>(b) | ((cq >> 2) << 2)) << off;
+            }
+            if (REC4) {
+                word |= (static_cast<uint32_t>(r.x) - base) << f.sh_e;
+                static_cast<uint32_t*>(out)[a0 + k] = word;
+            } else {
+                static_cast<int2*>(out)[a0 + k] = make_int2(r.x, static_cast<int>(word));
+            }
+        }
+    }
+}
+
+void build_lane_records(fea_plan* p, const DevBuf& trec, DevBuf& out, cudaStream_t s) {
+    out.reset();
+    if (!p->ln_ok || !trec.p) return;
+    const LaneFmt f = {{p->ln_wq[0], p->ln_wq[1], p->ln_wq[2]}, 6 + p->ln_wq[0] + p->ln_wq[1] + p->ln_wq[2]};
+    out.alloc(std::max<int64_t>(p->n_adj, 1) * (p->ln_rec4 ? 4 : 8));
+    auto kern = p->ln_rec4 ? k_lane_records<true> : k_lane_records<false>;
+    kern<<<grid_for(p->n_own * 32, 256), 256, 0, s>>>(p->trav_ptr.as<int64_t>(), reinterpret_cast<const int2*>(trec.p),
+                                                      p->ln_slot.as<uint8_t>(), p->ln_hdr.as<int4>(), p->n_own, f,
+                                                      out.p);
+    FEA_CK(cudaGetLastError());
+}
+
+void build_lane_slots(fea_plan* p, cudaStream_t s) {
+    p->ln_slot.reset();
+    p->ln_hdr.reset();
+    p->ln_rec.reset();
+    p->ln_recC.reset();
+    p->ln_ok = false;
+    p->ln_rec4 = false;
+    p->ln_q = 0;
+    if (!p->trav_rec.p || p->d != 1 || p->npe != 4 || p->dup_nodes || p->pos_bytes != 1 || p->trav_rw != 2 ||
+        p->max_cnt > 16 || p->max_adj >= 65536 || p->n_own == 0 || p->n_adj == 0 || p->kn.d1_no_lane)
+        return;
+    p->ln_slot.alloc(p->n_own * 16);
+    p->ln_hdr.alloc(p->n_own * 32);
+    DevBuf stats;
+    stats.alloc(6 * 4);
+    FEA_CK(cudaMemsetAsync(stats.p, 0, stats.bytes, s));
+    k_lane_colour<<<grid_for(p->n_own, 128), 128, 0, s>>>(
+        p->trav_ptr.as<int64_t>(), p->trav_meta.as<int64_t>(), reinterpret_cast<const int2*>(p->trav_rec.p),
+        p->n_own, p->ln_slot.as<uint8_t>(), p->ln_hdr.as<int4>(), stats.as<int>());
+    FEA_CK(cudaGetLastError());
+    int h[6] = {0, 0, 0, 0, 0, 0};
+    FEA_CK(cudaMemcpyAsync(h, stats.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaStreamSynchronize(s));
+    if (h[0] != 0) {
+        p->ln_slot.reset();
+        p->ln_hdr.reset();
+        return;
+    }
+    p->ln_ok = true;
+    p->ln_q = std::max(h[4], 1);
+    int bits = 6;
+    for (int c = 0; c < 3; ++c) {
+        p->ln_wq[c] = h[1 + c] <= 1 ? 0 : bits_for(static_cast<uint64_t>(h[1 + c] - 1));
+        bits += p->ln_wq[c];
+    }
+    // compact records when the entry offset fits next to the lane fields
+    p->ln_rec4 = !p->kn.d1_rec8 && static_cast<uint64_t>(h[5]) < (uint64_t{1} << (32 - bits));
+    build_lane_records(p, p->trav_rec, p->ln_rec, s);
 }
 
 void build_runs(fea_plan* p, cudaStream_t s) {
@@ -1165,6 +1379,7 @@ void build_colour_incidences(fea_plan* p, const std::vector<int32_t>& colour_of_
             static_cast<const uint32_t*>(p->posAC.p), pw, p->trav_rw, p->trav_ptr.as<int64_t>(), p->n_own,
             p->trav_recC.as<int32_t>());
         FEA_CK(cudaGetLastError());
+        build_lane_records(p, p->trav_recC, p->ln_recC, s);
     }
     FEA_CK(cudaStreamSynchronize(s));
 }
@@ -1177,7 +1392,8 @@ int64_t metadata_bytes(const fea_plan* p) {
                                 p->nrun_ptr.bytes + p->posA.bytes + p->posE.bytes +
                                 p->order.bytes + p->at_krow.bytes + p->at_rows.bytes + p->at_pos.bytes + p->colour_elems.bytes + p->adjC.bytes + p->posAC.bytes +
                                 p->node_order.bytes + p->trav_ptr.bytes + p->trav_meta.bytes +
-                                p->trav_rec.bytes + p->trav_recC.bytes + p->cnr_hdr.bytes + p->cnr_rec.bytes +
+                                p->trav_rec.bytes + p->trav_recC.bytes + p->ln_slot.bytes + p->ln_hdr.bytes +
+                                p->ln_rec.bytes + p->ln_recC.bytes + p->cnr_hdr.bytes + p->cnr_rec.bytes +
                                 p->cnr_recC.bytes + p->slot_hdr.bytes + p->slot_rec.bytes + p->slot_recC.bytes +
                                 p->pk_hdr.bytes + p->pk_krow.bytes + p->pk_cidx.bytes + p->pk_rows.bytes + p->pk_rowpair.bytes +
                                 p->pk_pairs.bytes);
@@ -1212,6 +1428,7 @@ fea_status fea_plan_create(int device, const int64_t* elem_dofs, int64_t n_eleme
         auto p = std::make_unique<fea_plan>();
         p->device = device;
         FEA_CK(cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device));
+        p->kn = read_knobs();
         p->cn_disabled = std::getenv("FEA_GATHER_NO_CN") != nullptr;
         p->d1_disabled = std::getenv("FEA_GATHER_NO_D1") != nullptr;
         p->slot_disabled = std::getenv("FEA_GATHER_NO_SLOT") != nullptr;
@@ -1305,6 +1522,7 @@ fea_status fea_plan_create_with_pattern(int device, const int64_t* elem_dofs, in
         auto p = std::make_unique<fea_plan>();
         p->device = device;
         FEA_CK(cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device));
+        p->kn = read_knobs();
         p->external = true;
         p->E_in = n_elements;
         p->m = m;

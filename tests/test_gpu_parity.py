@@ -577,8 +577,64 @@ def test_random_unstructured_meshes(gpu, orc, seed):
         assert close(plan.assemble(K, strategy="atomic").cpu().numpy(), want)
 
 
+def _check_d1(gpu, orc, conn, nn, ext=None):
+    """sorted / colour / accumulate / fused supplier of a d = 1 plan against the oracle"""
+    import torch
+    ed = M.element_dofs(conn, 1)
+    P = orc.Pattern.build(conn, nn, 1)
+    Kh = orc.fill_k(5, conn.shape[0], conn.shape[1])
+    K = torch.from_numpy(Kh).cuda()
+    if ext is None:
+        plan, S = gpu.Plan(ed, nn, dofs_per_node=1), P
+    else:
+        S = orc.Pattern.from_arrays(*ext)
+        plan = gpu.Plan.with_pattern(ed, nn, ext[0], ext[1], "csr")
+    want = S.assemble_sequential(ed, Kh)
+    with plan:
+        got = plan.assemble(K, strategy="sorted").cpu().numpy()
+        assert got.tobytes() == want.tobytes()
+        # accumulate continues the left fold from the existing values
+        v = torch.from_numpy(want.copy()).cuda()
+        plan.assemble(K, v, strategy="sorted", accumulate=True)
+        start = want.copy()
+        assert v.cpu().numpy().tobytes() == S.assemble_sequential(ed, Kh, values=start).tobytes()
+        col, _ = orc.greedy_colouring(conn, nn)
+        plan.set_colouring(col)
+        assert plan.assemble(K, strategy="colour").cpu().numpy().tobytes() == S.assemble_coloured(ed, Kh, col).tobytes()
+        assert close(plan.assemble(K, strategy="atomic").cpu().numpy(), want)
+
+
+def test_lane_owned_slots_shapes(gpu, orc):
+    """The d = 1, npe = 4 gather with lane-owned slots (k_gather_d1s) and its fall-backs:
+    structured tets and quads (every node's link is 3-colourable: compact 4-byte records), a
+    fan of 5 tets around an edge (the link of an edge end is an odd wheel: not 3-colourable, the
+    plan keeps the shared-memory fold), and a caller's superset pattern (slots no element
+    touches stay with lanes 1..3 and keep their start values)."""
+    for mesh, n, perm in [("tet4", 5, "nodes"), ("tet4", 3, None), ("quad4", 9, None), ("quad4", 7, "nodes")]:
+        conn, nn = M.make_mesh(mesh, n, perm)
+        _check_d1(gpu, orc, conn, nn)
+    fan = np.array([[0, 1, 2 + i, 2 + (i + 1) % 5] for i in range(5)], np.int64)
+    _check_d1(gpu, orc, fan, 7)
+    # fan glued to a structured block: one plan mixes colourable and non-colourable nodes
+    conn, nn = M.make_mesh("tet4", 2, None)
+    _check_d1(gpu, orc, np.concatenate([conn, fan + nn]), nn + 7)
+    # superset pattern on a small tet mesh: one extra column per row (rows stay <= 16 nodes)
+    conn, nn = M.make_mesh("tet4", 2, "nodes")
+    P = orc.Pattern.build(conn, nn, 1)
+    rp, cs = P.arrays()
+    rng = np.random.default_rng(9)
+    rows = []
+    for r in range(nn):
+        have = cs[rp[r]:rp[r + 1]]
+        extra = rng.choice(np.setdiff1d(np.arange(nn), have), size=1)
+        rows.append(np.unique(np.concatenate([have, extra])))
+    srp = np.concatenate([[0], np.cumsum([len(x) for x in rows])]).astype(np.int64)
+    _check_d1(gpu, orc, conn, nn, ext=(srp, np.concatenate(rows).astype(np.int64)))
+
+
 KERNEL_SWITCHES = ["FEA_SLOT_NO_FIXED", "FEA_CN_NO_RECORDS", "FEA_D1_NO_DIRECT", "FEA_D1_NO_VEC",
-                   "FEA_GATHER_NO_SLOT", "FEA_GATHER_NO_CN"]
+                   "FEA_GATHER_NO_SLOT", "FEA_GATHER_NO_CN", "FEA_D1_NO_LANE", "FEA_D1_REC8",
+                   "FEA_D1_NO_LANE,FEA_D1_NO_DIRECT"]
 
 
 @pytest.mark.parametrize("switch", KERNEL_SWITCHES)
@@ -596,7 +652,8 @@ def test_kernel_switches_same_bits(gpu, orc, switch, mesh, n, d, perm, monkeypat
     col, _ = orc.greedy_colouring(conn, nn)
     want_col = P.assemble_coloured(ed, Kh, col)
     K = torch.from_numpy(Kh).cuda()
-    monkeypatch.setenv(switch, "1")
+    for sw in switch.split(","):  # read when the plan is created
+        monkeypatch.setenv(sw, "1")
     with gpu.Plan(ed, n_rows, dofs_per_node=d) as plan:
         assert plan.assemble(K, strategy="sorted").cpu().numpy().tobytes() == want.tobytes()
         plan.set_colouring(col)

@@ -22,7 +22,7 @@ src = r'''
 template <int G, int U>
 __global__ void probe(const double* __restrict__ K, const int* __restrict__ rec, const long* __restrict__ tptr,
                       const long* __restrict__ vstart, const int* __restrict__ vlen, long n_nodes,
-                      double* __restrict__ out, const int* __restrict__ hi, long la) {
+                      double* __restrict__ out, const int* __restrict__ hi, long la, int wmode) {
     const long grp = (blockIdx.x * (long)blockDim.x + threadIdx.x) / G;
     const int gl = threadIdx.x % G;
     if (la > 0 && threadIdx.x == 0) {  // L2 prefetch frontier: rows first needed la nodes ahead
@@ -53,7 +53,10 @@ __global__ void probe(const double* __restrict__ K, const int* __restrict__ rec,
 #pragma unroll
         for (int u = 0; u < U; ++u) s += v[u];
     }
-    const long vb = vstart[grp];
+    // wmode 0: the real values rows (node-id order: random 120 B rows); 1: no writes (kept live);
+    // 2: the same rows written in traversal order (sequential)
+    const long vb = wmode == 2 ? grp * 16 : vstart[grp];
+    if (wmode == 1) { if (s == 1.2345e300) out[0] = s; return; }
     for (int i = gl; i < vlen[grp]; i += G) __stcs(out + vb + i, s + i);
 }
 // 8-byte records {entry, slot word} and a shared-memory fold (slot = byte gl of the word mod
@@ -94,12 +97,12 @@ void run_fold(torch::Tensor K, torch::Tensor rec2, torch::Tensor tptr, torch::Te
     else probe_fold<4, false, false><<<grid, 256>>>(K.data_ptr<double>(), (const int2*)rec2.data_ptr<int>(), tptr.data_ptr<long>(), vs.data_ptr<long>(), vl.data_ptr<int>(), n, out.data_ptr<double>());
 }
 void run(torch::Tensor K, torch::Tensor rec, torch::Tensor tptr, torch::Tensor vs, torch::Tensor vl, torch::Tensor out,
-         int g, int u, int bs, torch::Tensor hi, long la) {
+         int g, int u, int bs, torch::Tensor hi, long la, int wmode) {
     long n = vl.numel();
     long threads = n * g;
     int grid = (threads + bs - 1) / bs;
     auto args = [&](auto kern) { kern<<<grid, bs>>>(K.data_ptr<double>(), rec.data_ptr<int>(), tptr.data_ptr<long>(),
-        vs.data_ptr<long>(), vl.data_ptr<int>(), n, out.data_ptr<double>(), hi.data_ptr<int>(), la); };
+        vs.data_ptr<long>(), vl.data_ptr<int>(), n, out.data_ptr<double>(), hi.data_ptr<int>(), la, wmode); };
     if (g == 4 && u == 4) args(probe<4, 4>);
     if (g == 4 && u == 8) args(probe<4, 8>);
     if (g == 4 && u == 24) args(probe<4, 24>);
@@ -108,7 +111,7 @@ void run(torch::Tensor K, torch::Tensor rec, torch::Tensor tptr, torch::Tensor v
     if (g == 2 && u == 24) args(probe<2, 24>);
 }
 '''
-mod = load_inline("probe_d1", cpp_sources="void run(torch::Tensor K, torch::Tensor rec, torch::Tensor tptr, torch::Tensor vs, torch::Tensor vl, torch::Tensor out, int g, int u, int bs, torch::Tensor hi, long la); void run_fold(torch::Tensor K, torch::Tensor rec2, torch::Tensor tptr, torch::Tensor vs, torch::Tensor vl, torch::Tensor out, int smem);",
+mod = load_inline("probe_d1", cpp_sources="void run(torch::Tensor K, torch::Tensor rec, torch::Tensor tptr, torch::Tensor vs, torch::Tensor vl, torch::Tensor out, int g, int u, int bs, torch::Tensor hi, long la, int wmode); void run_fold(torch::Tensor K, torch::Tensor rec2, torch::Tensor tptr, torch::Tensor vs, torch::Tensor vl, torch::Tensor out, int smem);",
                   cuda_sources=src, functions=["run", "run_fold"],
                   extra_cuda_cflags=["-gencode", "arch=compute_100a,code=sm_100a", "-O3"], verbose=False)
 
@@ -131,7 +134,7 @@ rp, _ = plan.csr()
 vs = rp[:-1][trav].astype(np.int64)
 vl = np.diff(rp)[trav].astype(np.int32)
 K = fea.fill_seeded_k(E, 4, 42)
-out = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+out = torch.empty(max(plan.nnz, 16 * nn + 16), dtype=torch.float64, device="cuda")
 T = [torch.from_numpy(x).cuda() for x in (rec, tptr, vs, vl)]
 last = rec[np.maximum(tptr[1:] - 1, 0)]                          # highest K row per traversal node
 hi = torch.from_numpy(np.maximum.accumulate(last).astype(np.int32)).cuda()
@@ -139,19 +142,19 @@ words = (rec.astype(np.uint64) * np.uint64(2654435761) >> np.uint64(7)).astype(n
 rec2 = torch.from_numpy(np.stack([rec, words], axis=1).reshape(-1).copy()).cuda()
 alg = 8 * E * 16 + 8 * plan.nnz + 4 * E * npe
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-for g, u, bs, la in [(4, 4, 256, 0), (2, 8, 128, 0), (4, 4, 256, 8192), (4, 4, 256, 32768)]:
-            mod.run(K, *T, out, g, u, bs, hi, la)
+for g, u, bs, la, wm in [(4, 4, 256, 0, 0), (4, 4, 256, 0, 1), (4, 4, 256, 0, 2), (2, 8, 128, 0, 0), (4, 4, 256, 8192, 0)]:
+            mod.run(K, *T, out, g, u, bs, hi, la, wm)
             ms = []
             for _ in range(5):
                 flush.zero_()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                mod.run(K, *T, out, g, u, bs, hi, la)
+                mod.run(K, *T, out, g, u, bs, hi, la, wm)
                 e1.record()
                 torch.cuda.synchronize()
                 ms.append(e0.elapsed_time(e1))
             t = float(np.mean(ms))
-            print(f"G={g} U={u:2d} bs={bs} prefetch-ahead={la}: {t:.3f} ms  ({alg / t / 1e6:.0f} GB/s algorithmic)", flush=True)
+            print(f"G={g} U={u:2d} bs={bs} prefetch-ahead={la} writes={("rows", "none", "sequential")[wm]}: {t:.3f} ms  ({alg / t / 1e6:.0f} GB/s algorithmic)", flush=True)
 
 for smem in (0, 1, 2, 3):
     mod.run_fold(K, rec2, T[1], T[2], T[3], out, smem)
