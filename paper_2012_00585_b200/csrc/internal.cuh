@@ -61,6 +61,8 @@ struct DeviceScope {
 struct Knobs {
     bool atomic_legacy, atomic_no_patch, slot_no_fixed, cn_unpacked, cn_no_records, d1_no_direct, d1_no_vec;
     bool d1_no_lane;  // FEA_D1_NO_LANE: shared-memory fold (k_gather_d1g) instead of lane-owned slots
+    bool patch_tickets;  // FEA_PATCH_TICKETS: tickets also for short runs
+    bool patch_static;  // FEA_PATCH_STATIC: k_atomic_patch CTAs stride by the grid size instead of taking tickets
     bool d1_rec8;  // FEA_D1_REC8: 8-byte lane records even where the compact 4-byte form fits
     int d1_acc_mod, d1v_acc_mod;  // accumulator stride residues (mod 16 doubles)
 };
@@ -139,6 +141,8 @@ struct fea_plan {
     feagpu::DevBuf pk_rowpair;  // int32 [] first pair of the row | pair count << 16 (pairs sorted by row)
     feagpu::DevBuf pk_pairs;  // uint16 [] row index << 8 | position per distinct pair
     int64_t pk_n = 0;
+    feagpu::DevBuf pk_ticket;  // uint64 [1024] patch ticket counters, one per launch in flight (ring)
+    uint32_t pk_ticket_next = 0;
     int32_t pk_max_pairs = 0;
     feagpu::DevBuf node_order;  // int32 [n_own] gather traversal order (empty: node id order)
     // d = 1 with a traversal order: the sorted incidences re-laid in traversal order, so the

@@ -1781,7 +1781,7 @@ __global__ void __launch_bounds__(kPatchWarps * 32)
     k_atomic_patch(const double* __restrict__ K, const int4* __restrict__ hdr, const int32_t* __restrict__ pk_krow,
                    const uint16_t* __restrict__ pk_cidx, const int64_t* __restrict__ pk_rows,
                    const int32_t* __restrict__ pk_rowpair, const uint16_t* __restrict__ pk_pairs, int64_t n_patch,
-                   int acc_doubles, double* __restrict__ values) {
+                   int acc_doubles, unsigned long long* __restrict__ ticket, double* __restrict__ values) {
     constexpr int M = D * NPE, MM = M * M, DD = D * D, NN = NPE * NPE;
     constexpr int KB = MM * 8, CB = NN * 2, SLOT = KB + CB;
     constexpr int NT = kPatchWarps * 32;
@@ -1800,26 +1800,44 @@ __global__ void __launch_bounds__(kPatchWarps * 32)
     int32_t* s_rowpair = reinterpret_cast<int32_t*>(s_rows + MAXR);
     uint16_t* s_pairs = reinterpret_cast<uint16_t*>(s_rowpair + MAXR);
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_pairs + MAXP);  // one mbarrier per stage
+    // patches are handed out in order by a ticket counter (zeroed by the launcher): persistent
+    // CTAs striding by gridDim drift apart over thousands of patches, and the values rows that
+    // neighbouring patches share (the next row of patches, 128 patches later on config 5) have
+    // left L2 by the time the slower CTA reaches them. The issue cursor claims a patch, the
+    // fold cursor picks it up from s_q a few slots later. ticket == nullptr: static stride (A/B).
+    int64_t* s_q = reinterpret_cast<int64_t*>(bars + STAGES);  // 4 patch ids, issue -> fold cursor
     int64_t m_row = 0;
     int32_t m_rowpair = 0;
     uint16_t m_pair[PPT];
     const int64_t G = gridDim.x;
-    if (static_cast<int64_t>(blockIdx.x) >= n_patch) return;
+    int qw = 0, qr = 0;
+    // thread 0 holds the ticket of the patch after the one its issue cursor is in, so the
+    // counter's round trip (~1 us, 10 % of a patch on cfg2) is off the issue path
+    auto ticket_next = [&](int64_t stride_next) -> int64_t {
+        return ticket ? static_cast<int64_t>(atomicAdd(ticket, 1ull)) : stride_next;
+    };
+    int64_t ipt = 0, ipt_next = 0;
     if (tid == 0) {
         for (int st = 0; st < STAGES; ++st) mbar_init(smem_u32(bars + st), 1);
         mbar_fence_init();
+        ipt = ticket_next(blockIdx.x);
+        ipt_next = ticket_next(ipt + G);
+        s_q[qw++ & 3] = ipt;
     }
     __syncthreads();
+    int64_t pt = s_q[qr++ & 3];
+    if (pt >= n_patch) return;
     // K is read once: L2 evict-first for its bulk copies keeps the values lines being reduced
     // into resident (created per copy: a hoisted createpolicy was miscompiled, see above)
     // issue cursor (STAGES - 1 element slots ahead of the fold): patch and slot. Thread 0
     // copies a slot's K block (4.6 KB contiguous) and its pair indices with two bulk copies.
-    int64_t ipt = blockIdx.x;
     int ik = 0;
     auto advance = [&]() {
         if (++ik == P) {
             ik = 0;
-            ipt += G;
+            ipt = ipt_next;
+            s_q[qw++ & 3] = ipt;
+            ipt_next = ticket_next(ipt + G);
         }
     };
     auto krow_at = [&]() -> int32_t { return ipt < n_patch ? __ldg(pk_krow + ipt * P + ik) : -1; };
@@ -1864,7 +1882,6 @@ __global__ void __launch_bounds__(kPatchWarps * 32)
         kr_next = krow_at();
     }
     int4 h = make_int4(0, 0, 0, 0);
-    int64_t pt = blockIdx.x;
     int k = 0, stage = 0;
     uint32_t phase = 0;  // bit st: parity of stage st's next completion
     for (; pt < n_patch;) {
@@ -1897,15 +1914,25 @@ __global__ void __launch_bounds__(kPatchWarps * 32)
             const unsigned char* kb = sb + tid * 8;
             const unsigned char* cb = sb + KB;
             unsigned char* ab = reinterpret_cast<unsigned char*>(acc);
+            // within one element the (a, b) pairs are distinct, so a thread's T entries land in T
+            // different accumulator slots (or in the spare pair, never flushed): all index and K
+            // loads first, then the accumulator loads, then the stores - one shared-memory round
+            // trip per phase instead of a load -> add -> store chain per entry (ncu, config 5:
+            // 30 % of the stall samples on those chains, 20 % on the barrier that waits for them)
+            double kv[T], av[T];
+            double* ap[T];
 #pragma unroll
             for (int t = 0; t < T; ++t) {
-                if (t < T - 1 || MM % NT == 0 || tid + NT * t < MM) {
-                    const uint32_t c = *reinterpret_cast<const uint16_t*>(cb + cio[t]);
-                    const double kv = *reinterpret_cast<const double*>(kb + t * NT * 8);
-                    double* a = reinterpret_cast<double*>(ab + c * (DD * 8) + co8[t]);
-                    *a += kv;
-                }
+                const bool on = t < T - 1 || MM % NT == 0 || tid + NT * t < MM;
+                const uint32_t c = on ? *reinterpret_cast<const uint16_t*>(cb + cio[t]) : 0u;
+                kv[t] = on ? *reinterpret_cast<const double*>(kb + t * NT * 8) : 0.0;
+                ap[t] = reinterpret_cast<double*>(ab + c * (DD * 8) + co8[t]);
             }
+#pragma unroll
+            for (int t = 0; t < T; ++t) av[t] = *ap[t];
+#pragma unroll
+            for (int t = 0; t < T; ++t)
+                if (t < T - 1 || MM % NT == 0 || tid + NT * t < MM) *ap[t] = av[t] + kv[t];
         }
         if (k == P - 1) {  // patch end: a warp per row, one RED per distinct slot
             const int n_rows = (h.w >> 8) & 0xff;
@@ -1938,7 +1965,7 @@ __global__ void __launch_bounds__(kPatchWarps * 32)
         stage = (stage + 1) % STAGES;
         if (++k == P) {
             k = 0;
-            pt += G;
+            pt = s_q[qr++ & 3];  // claimed STAGES - 1 slots (and several barriers) ago
         }
     }
 }
@@ -2640,21 +2667,32 @@ void run_atomic_cta(fea_plan* p, const double* K, double* values, cudaStream_t s
 #ifndef FEA_PATCH_STAGES
 #define FEA_PATCH_STAGES 4
 #endif
+constexpr int kTicketRing = 1024;
 template <int D>
 void run_atomic_patch(fea_plan* p, const double* K, double* values, cudaStream_t s) {
     constexpr int NPE = 8, P = kPatchElems, STAGES = FEA_PATCH_STAGES;
     constexpr int SLOT = D * NPE * D * NPE * 8 + NPE * NPE * 2;
     const int acc_doubles = ((p->pk_max_pairs + 1) * D * D + 1) & ~1;  // + spare pair; 16-byte aligned stages
     const size_t smem = static_cast<size_t>(acc_doubles) * 8 + STAGES * SLOT +
-                        static_cast<size_t>(P * NPE) * 12 + static_cast<size_t>(P * NPE * NPE) * 2 + STAGES * 8;
+                        static_cast<size_t>(P * NPE) * 12 + static_cast<size_t>(P * NPE * NPE) * 2 + STAGES * 8 + 32;
     FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "patch accumulator too large");
     auto kern = k_atomic_patch<D, NPE, P, STAGES>;
     const int per_sm = launch_prep(p, kern, kPatchWarps * 32, smem);
     const int64_t blocks = std::min<int64_t>(p->pk_n, static_cast<int64_t>(p->sms) * std::max(per_sm, 1));
     if (blocks == 0) return;
+    // one ticket counter per launch, from a ring (assemblies of one plan on several streams,
+    // or several launches captured in one graph, must not share a live counter)
+    // (long runs only: on cfg2, 44 patches per CTA, tickets measured 0.463 vs 0.444 ms - CTAs
+    // that start together then flush the rows their neighbouring patches share at the same time)
+    unsigned long long* ticket = nullptr;
+    if (!p->kn.patch_static && (p->kn.patch_tickets || p->pk_n >= 256 * blocks)) {
+        if (!p->pk_ticket.p) p->pk_ticket.alloc(kTicketRing * 8);
+        ticket = p->pk_ticket.as<unsigned long long>() + (p->pk_ticket_next++ % kTicketRing);
+        FEA_CK(cudaMemsetAsync(ticket, 0, 8, s));
+    }
     kern<<<static_cast<unsigned>(blocks), kPatchWarps * 32, smem, s>>>(
         K, p->pk_hdr.as<int4>(), p->pk_krow.as<int32_t>(), p->pk_cidx.as<uint16_t>(), p->pk_rows.as<int64_t>(),
-        p->pk_rowpair.as<int32_t>(), p->pk_pairs.as<uint16_t>(), p->pk_n, acc_doubles, values);
+        p->pk_rowpair.as<int32_t>(), p->pk_pairs.as<uint16_t>(), p->pk_n, acc_doubles, ticket, values);
     FEA_CK(cudaGetLastError());
     p->last_launches += 1;
 }

@@ -163,6 +163,80 @@ void build_patches(fea_plan* p, cudaStream_t s) {
         ++pid;
     }
     const int64_t n_patch = pid;
+    // Tiled visit order for lattice-like patch sequences (a structured mesh in lexicographic
+    // order: patch q shares nodes with q + 1, q + s1 +- 1, q + s2 +- s1 +- 1). In sequence order
+    // the patches of the next plane come s2 patches later (config 5: 16,384 patches = 0.6 GB of
+    // K), so the values rows of every node plane between two patch planes are fetched and
+    // written back twice. Visiting tiles of T x T patch columns plane after plane brings the next
+    // plane's patches T * T tickets later. The strides are detected from the patch adjacency
+    // (no geometry in the plan); any other sequence keeps its order. Any order is valid.
+    if (n_patch > 0 && !std::getenv("FEA_PATCH_NO_TILES")) {
+        std::vector<int32_t> patch_of(E, -1);
+        for (int64_t q = 0; q < n_patch; ++q)
+            for (int k = 0; k < P; ++k)
+                if (members[q * P + k] >= 0) patch_of[members[q * P + k]] = static_cast<int32_t>(q);
+        std::vector<int64_t> offs;
+        auto later_neighbours = [&](int64_t q) {
+            offs.clear();
+            for (int k = 0; k < P; ++k) {
+                const int32_t le = members[q * P + k];
+                if (le < 0) continue;
+                for (int a = 0; a < NPE; ++a) {
+                    const int32_t v = node(le, a);
+                    for (int64_t j = aptr[v]; j < aptr[v + 1]; ++j) {
+                        const int64_t nb = patch_of[aelem[j]];
+                        if (nb > q) offs.push_back(nb - q);
+                    }
+                }
+            }
+            std::sort(offs.begin(), offs.end());
+            offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+        };
+        int64_t s1 = 0, s2 = 0;
+        for (int smp = 0; smp < 64 && s1 == 0; ++smp) {  // an interior patch: 13 later neighbours
+            later_neighbours(n_patch / 2 + (n_patch / 131) * smp % std::max<int64_t>(n_patch / 2, 1));
+            if (offs.size() == 13 && offs[0] == 1 && offs[1] + 1 == offs[2] && offs[2] + 1 == offs[3]) {
+                s1 = offs[2];
+                s2 = offs[8];
+            }
+        }
+        bool lattice = s1 > 1 && s2 > s1 && s2 % s1 == 0 && n_patch >= 2 * s2;
+        if (lattice) {
+            const int64_t want[13] = {1, s1 - 1, s1, s1 + 1, s2 - s1 - 1, s2 - s1, s2 - s1 + 1, s2 - 1, s2, s2 + 1,
+                                      s2 + s1 - 1, s2 + s1, s2 + s1 + 1};
+            for (int smp = 0; smp < 257 && lattice; ++smp) {
+                later_neighbours((n_patch - 1) * smp / 256);
+                for (int64_t o : offs) lattice = lattice && std::find(want, want + 13, o) != want + 13;
+            }
+        }
+        // only where a plane of patches outgrows the L2 (K bytes of one plane)
+        const int64_t plane_k = s2 * P * static_cast<int64_t>(p->m) * p->m * 8;
+        if (std::getenv("FEA_PATCH_DEBUG"))
+            std::fprintf(stderr, "patch lattice: n_patch %lld offs %zu s1 %lld s2 %lld lattice %d plane_k %lld\n",
+                         (long long)n_patch, offs.size(), (long long)s1, (long long)s2, (int)lattice, (long long)plane_k);
+        const char* tile_env = std::getenv("FEA_PATCH_TILE");
+        if (lattice && (plane_k > (int64_t{64} << 20) || tile_env)) {
+            int T = 16;
+            if (tile_env) T = std::max(1, std::atoi(tile_env));
+            const int64_t nx = s1, ny = s2 / s1, tiles_x = (nx + T - 1) / T;
+            std::vector<std::pair<uint64_t, int32_t>> key(static_cast<size_t>(n_patch));
+            for (int64_t q = 0; q < n_patch; ++q) {
+                const int64_t x = q % s1, y = (q % s2) / s1, z = q / s2;
+                const uint64_t tile = static_cast<uint64_t>((y / T) * tiles_x + x / T);
+                key[q] = {(tile << 40) | (static_cast<uint64_t>(z) << 20) |
+                              static_cast<uint64_t>((y % T) * T + x % T),
+                          static_cast<int32_t>(q)};
+            }
+            if (tiles_x * ((ny + T - 1) / T) < (int64_t{1} << 23) && n_patch / s2 < (int64_t{1} << 20) && T * T < (1 << 20)) {
+                std::sort(key.begin(), key.end());
+                std::vector<int32_t> m2(members.size());
+                for (int64_t q = 0; q < n_patch; ++q)
+                    std::copy(members.begin() + static_cast<int64_t>(key[q].second) * P,
+                              members.begin() + static_cast<int64_t>(key[q].second + 1) * P, m2.begin() + q * P);
+                members.swap(m2);
+            }
+        }
+    }
     // per patch: rows, pairs, element pair indices
     std::vector<int32_t> hk(static_cast<size_t>(n_patch * P), -1);
     std::vector<uint16_t> hc(static_cast<size_t>(n_patch * P * NN), 0xffffu);
