@@ -187,7 +187,8 @@ def rank_nodes(conn, n_nodes: int, world: int, rank: int):
 
 KERNEL_NAMES = {
     "sorted": "k_gather_slot<3,8> (warp = node, lane = slot, register accumulators, TMA bulk copies)",
-    "atomic": "k_atomic_staged<3,8,u8> (visit-order metadata, cp.async-staged K, RED.E.ADD.F64)",
+    "atomic": "k_atomic_patch<3,8,8,4> (2x2x2 element patches pre-reduced in shared memory, TMA bulk staging, "
+              "one RED.E.ADD.F64 per distinct slot, patches by ticket in a tiled order)",
     "colour": "k_gather_slot<3,8> (colour-ordered incidences)",
     "colour_passes": "k_scatter<32,u8,plain> x n_colours",
 }

@@ -5,7 +5,7 @@
 set -u
 OUT=${OUT:-gpurun_out}
 python tools/prof_case.py --cfg 5 --strategies sorted,atomic --iters 1 > $OUT/cfg5_case.log 2>&1 || { echo "case failed"; exit 1; }
-for spec in sorted:k_gather_slot atomic:k_atomic_staged; do
+for spec in sorted:k_gather_slot atomic:k_atomic_patch; do
   s=${spec%%:*}; k=${spec##*:}
   timeout 1200 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 \
       -o $OUT/r02_ncu_cfg5_$s -f python tools/prof_case.py --cfg 5 --strategies $s --iters 1 \
