@@ -194,7 +194,7 @@ void build_patches(fea_plan* p, cudaStream_t s) {
         };
         int64_t s1 = 0, s2 = 0;
         for (int smp = 0; smp < 64 && s1 == 0; ++smp) {  // an interior patch: 13 later neighbours
-            later_neighbours(n_patch / 2 + (n_patch / 131) * smp % std::max<int64_t>(n_patch / 2, 1));
+            later_neighbours((n_patch / 2 + smp * (std::max<int64_t>(n_patch / 67, 1) | 1)) % n_patch);
             if (offs.size() == 13 && offs[0] == 1 && offs[1] + 1 == offs[2] && offs[2] + 1 == offs[3]) {
                 s1 = offs[2];
                 s2 = offs[8];

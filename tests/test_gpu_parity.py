@@ -632,6 +632,31 @@ def test_lane_owned_slots_shapes(gpu, orc):
     _check_d1(gpu, orc, conn, nn, ext=(srp, np.concatenate(rows).astype(np.int64)))
 
 
+@pytest.mark.parametrize("env", [{"FEA_PATCH_TICKETS": "1"}, {"FEA_PATCH_TICKETS": "1", "FEA_PATCH_TILE": "2"},
+                                 {"FEA_PATCH_STATIC": "1", "FEA_PATCH_TILE": "3"}, {"FEA_PATCH_NO_TILES": "1"}])
+@pytest.mark.parametrize("n,perm", [(8, None), (7, None), (6, "elements")])
+def test_atomic_patch_schedules(gpu, orc, env, n, perm, monkeypatch):
+    """k_atomic_patch under every patch schedule: tickets / grid stride, lattice tiles of several
+    sizes (forced on a small lexicographic mesh, where the detection finds s1 = n/2, s2 = (n/2)^2)
+    or the sequence order. Any order is a valid atomic assembly: within the reference tolerance of
+    the sequential result, and bitwise with ones (every sum is exact)."""
+    import torch
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    conn, nn, ed, n_rows = problem("hex8", n, 3, perm)
+    E, m = ed.shape
+    P = orc.Pattern.build(conn, nn, 3)
+    Kh = orc.fill_k(3, E, m)
+    want = P.assemble_sequential(ed, Kh)
+    ones = np.ones_like(Kh)
+    want1 = P.assemble_sequential(ed, ones)
+    with gpu.Plan(ed, n_rows, dofs_per_node=3) as plan:
+        for _ in range(2):  # the second launch takes the next ticket counter of the ring
+            assert close(plan.assemble(torch.from_numpy(Kh).cuda(), strategy="atomic").cpu().numpy(), want)
+        got1 = plan.assemble(torch.from_numpy(ones).cuda(), strategy="atomic").cpu().numpy()
+        assert got1.tobytes() == want1.tobytes()
+
+
 KERNEL_SWITCHES = ["FEA_SLOT_NO_FIXED", "FEA_CN_NO_RECORDS", "FEA_D1_NO_DIRECT", "FEA_D1_NO_VEC",
                    "FEA_GATHER_NO_SLOT", "FEA_GATHER_NO_CN", "FEA_D1_NO_LANE", "FEA_D1_REC8",
                    "FEA_D1_NO_LANE,FEA_D1_NO_DIRECT"]
