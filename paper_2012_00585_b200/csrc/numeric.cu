@@ -22,6 +22,58 @@ namespace feagpu {
 void build_atomic_maps(fea_plan* p, cudaStream_t s);
 void build_patches(fea_plan* p, cudaStream_t s);
 
+// --- lattice-like item sequences and their tiled visit order ----------------------------------
+// Items (the patches of k_atomic_patch) in visit order. On a structured
+// mesh in lexicographic order item q shares nodes with q + 1, q + s1 +- 1, q + s1, q + s2 +- s1 +- 1,
+// ...: the strides are read off an interior item's later neighbours and checked on 257 samples
+// (no geometry in the plan). later(q, out) fills the sorted distinct offsets nb - q of the items
+// nb > q that share a node with q.
+template <class Later>
+bool detect_lattice(int64_t n, Later&& later, int64_t* s1_out, int64_t* s2_out) {
+    std::vector<int64_t> offs;
+    int64_t s1 = 0, s2 = 0;
+    for (int smp = 0; smp < 64 && s1 == 0 && n > 0; ++smp) {  // an interior item: 13 later neighbours
+        later((n / 2 + smp * (std::max<int64_t>(n / 67, 1) | 1)) % n, offs);
+        if (offs.size() == 13 && offs[0] == 1 && offs[1] + 1 == offs[2] && offs[2] + 1 == offs[3]) {
+            s1 = offs[2];
+            s2 = offs[8];
+        }
+    }
+    bool lattice = s1 > 1 && s2 > s1 && s2 % s1 == 0 && n >= 2 * s2;
+    if (lattice) {
+        const int64_t want[13] = {1, s1 - 1, s1, s1 + 1, s2 - s1 - 1, s2 - s1, s2 - s1 + 1, s2 - 1, s2, s2 + 1,
+                                  s2 + s1 - 1, s2 + s1, s2 + s1 + 1};
+        for (int smp = 0; smp < 257 && lattice; ++smp) {
+            later((n - 1) * smp / 256, offs);
+            for (int64_t o : offs) lattice = lattice && std::find(want, want + 13, o) != want + 13;
+        }
+    }
+    *s1_out = s1;
+    *s2_out = s2;
+    return lattice;
+}
+
+// Sequence positions re-ordered into tiles of T x T columns visited plane after plane: the items
+// of the next plane follow T * T positions later instead of s2 (a whole plane, which outgrows
+// the L2 on large meshes, so every values row shared between two planes was fetched twice).
+std::vector<int32_t> tiled_sequence(int64_t n, int64_t s1, int64_t s2, int T) {
+    const int64_t nx = s1, ny = s2 / s1, tiles_x = (nx + T - 1) / T;
+    std::vector<int32_t> seq(static_cast<size_t>(n));
+    for (int64_t q = 0; q < n; ++q) seq[q] = static_cast<int32_t>(q);
+    if (tiles_x * ((ny + T - 1) / T) >= (int64_t{1} << 23) || n / s2 >= (int64_t{1} << 20) || T * T >= (1 << 20))
+        return seq;
+    std::vector<std::pair<uint64_t, int32_t>> key(static_cast<size_t>(n));
+    for (int64_t q = 0; q < n; ++q) {
+        const int64_t x = q % s1, y = (q % s2) / s1, z = q / s2;
+        const uint64_t tile = static_cast<uint64_t>((y / T) * tiles_x + x / T);
+        key[q] = {(tile << 40) | (static_cast<uint64_t>(z) << 20) | static_cast<uint64_t>((y % T) * T + x % T),
+                  static_cast<int32_t>(q)};
+    }
+    std::sort(key.begin(), key.end());
+    for (int64_t q = 0; q < n; ++q) seq[q] = key[q].second;
+    return seq;
+}
+
 void ensure_element_maps(fea_plan* p, cudaStream_t s) {
     if (p->posE.p && p->order.p) return;
     const int64_t n = p->E * p->npe * p->npe;
@@ -175,8 +227,7 @@ void build_patches(fea_plan* p, cudaStream_t s) {
         for (int64_t q = 0; q < n_patch; ++q)
             for (int k = 0; k < P; ++k)
                 if (members[q * P + k] >= 0) patch_of[members[q * P + k]] = static_cast<int32_t>(q);
-        std::vector<int64_t> offs;
-        auto later_neighbours = [&](int64_t q) {
+        auto later = [&](int64_t q, std::vector<int64_t>& offs) {
             offs.clear();
             for (int k = 0; k < P; ++k) {
                 const int32_t le = members[q * P + k];
@@ -193,48 +244,21 @@ void build_patches(fea_plan* p, cudaStream_t s) {
             offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
         };
         int64_t s1 = 0, s2 = 0;
-        for (int smp = 0; smp < 64 && s1 == 0; ++smp) {  // an interior patch: 13 later neighbours
-            later_neighbours((n_patch / 2 + smp * (std::max<int64_t>(n_patch / 67, 1) | 1)) % n_patch);
-            if (offs.size() == 13 && offs[0] == 1 && offs[1] + 1 == offs[2] && offs[2] + 1 == offs[3]) {
-                s1 = offs[2];
-                s2 = offs[8];
-            }
-        }
-        bool lattice = s1 > 1 && s2 > s1 && s2 % s1 == 0 && n_patch >= 2 * s2;
-        if (lattice) {
-            const int64_t want[13] = {1, s1 - 1, s1, s1 + 1, s2 - s1 - 1, s2 - s1, s2 - s1 + 1, s2 - 1, s2, s2 + 1,
-                                      s2 + s1 - 1, s2 + s1, s2 + s1 + 1};
-            for (int smp = 0; smp < 257 && lattice; ++smp) {
-                later_neighbours((n_patch - 1) * smp / 256);
-                for (int64_t o : offs) lattice = lattice && std::find(want, want + 13, o) != want + 13;
-            }
-        }
+        const bool lattice = detect_lattice(n_patch, later, &s1, &s2);
         // only where a plane of patches outgrows the L2 (K bytes of one plane)
         const int64_t plane_k = s2 * P * static_cast<int64_t>(p->m) * p->m * 8;
         if (std::getenv("FEA_PATCH_DEBUG"))
-            std::fprintf(stderr, "patch lattice: n_patch %lld offs %zu s1 %lld s2 %lld lattice %d plane_k %lld\n",
-                         (long long)n_patch, offs.size(), (long long)s1, (long long)s2, (int)lattice, (long long)plane_k);
+            std::fprintf(stderr, "patch lattice: n_patch %lld s1 %lld s2 %lld lattice %d plane_k %lld\n",
+                         (long long)n_patch, (long long)s1, (long long)s2, (int)lattice, (long long)plane_k);
         const char* tile_env = std::getenv("FEA_PATCH_TILE");
         if (lattice && (plane_k > (int64_t{64} << 20) || tile_env)) {
-            int T = 16;
-            if (tile_env) T = std::max(1, std::atoi(tile_env));
-            const int64_t nx = s1, ny = s2 / s1, tiles_x = (nx + T - 1) / T;
-            std::vector<std::pair<uint64_t, int32_t>> key(static_cast<size_t>(n_patch));
-            for (int64_t q = 0; q < n_patch; ++q) {
-                const int64_t x = q % s1, y = (q % s2) / s1, z = q / s2;
-                const uint64_t tile = static_cast<uint64_t>((y / T) * tiles_x + x / T);
-                key[q] = {(tile << 40) | (static_cast<uint64_t>(z) << 20) |
-                              static_cast<uint64_t>((y % T) * T + x % T),
-                          static_cast<int32_t>(q)};
-            }
-            if (tiles_x * ((ny + T - 1) / T) < (int64_t{1} << 23) && n_patch / s2 < (int64_t{1} << 20) && T * T < (1 << 20)) {
-                std::sort(key.begin(), key.end());
-                std::vector<int32_t> m2(members.size());
-                for (int64_t q = 0; q < n_patch; ++q)
-                    std::copy(members.begin() + static_cast<int64_t>(key[q].second) * P,
-                              members.begin() + static_cast<int64_t>(key[q].second + 1) * P, m2.begin() + q * P);
-                members.swap(m2);
-            }
+            const int T = tile_env ? std::max(1, std::atoi(tile_env)) : 16;
+            const std::vector<int32_t> seq = tiled_sequence(n_patch, s1, s2, T);
+            std::vector<int32_t> m2(members.size());
+            for (int64_t q = 0; q < n_patch; ++q)
+                std::copy(members.begin() + static_cast<int64_t>(seq[q]) * P,
+                          members.begin() + static_cast<int64_t>(seq[q] + 1) * P, m2.begin() + q * P);
+            members.swap(m2);
         }
     }
     // per patch: rows, pairs, element pair indices
