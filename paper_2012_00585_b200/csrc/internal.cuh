@@ -61,6 +61,7 @@ struct DeviceScope {
 struct Knobs {
     bool atomic_legacy, atomic_no_patch, slot_no_fixed, cn_unpacked, cn_no_records, d1_no_direct, d1_no_vec;
     bool d1_no_lane;  // FEA_D1_NO_LANE: shared-memory fold (k_gather_d1g) instead of lane-owned slots
+    bool atomic_no_strip;  // FEA_ATOMIC_NO_STRIP: k_atomic_staged instead of strip pre-reduction (npe 4, d 1)
     bool patch_tickets;  // FEA_PATCH_TICKETS: tickets also for short runs
     bool patch_static;  // FEA_PATCH_STATIC: k_atomic_patch CTAs stride by the grid size instead of taking tickets
     bool d1_rec8;  // FEA_D1_REC8: 8-byte lane records even where the compact 4-byte form fits
@@ -141,6 +142,15 @@ struct fea_plan {
     feagpu::DevBuf pk_rowpair;  // int32 [] first pair of the row | pair count << 16 (pairs sorted by row)
     feagpu::DevBuf pk_pairs;  // uint16 [] row index << 8 | position per distinct pair
     int64_t pk_n = 0;
+    // atomic route for npe = 4, d = 1 (k_atomic_strip; lazy): strips of 48 consecutive elements of
+    // the visit order, per strip the distinct (row node, position) pairs and for each pair the
+    // list of K entries of the strip that feed it (fixed-stride blob, one bulk copy per strip)
+    feagpu::DevBuf sk_meta;   // [sk_n][sk_stride] header, values start per local node, position per pair
+    feagpu::DevBuf sk_shape;  // [shapes][sk_sh_stride] list end per pair, local row per pair, entry offsets
+    feagpu::DevBuf sk_k0;     // int4 [sk_n] {first K row if the strip's K rows are consecutive else -1, elements, shape}
+    feagpu::DevBuf sk_krow;   // int32 [sk_n*48] K row per element (-1: none)
+    int64_t sk_n = 0;
+    int32_t sk_stride = 0, sk_off_pos = 0, sk_sh_stride = 0, sk_off_prow = 0, sk_off_ent = 0;
     feagpu::DevBuf pk_ticket;  // uint64 [1024] patch ticket counters, one per launch in flight (ring)
     uint32_t pk_ticket_next = 0;
     int32_t pk_max_pairs = 0;

@@ -2120,6 +2120,109 @@ __global__ void k_fill_k(double* __restrict__ K, int64_t n, int m, uint64_t seed
     }
 }
 
+// ---------------------------------------------------------------------------
+// FEA_ATOMIC for npe = 4, d = 1 (tet4 / quad4 scalar problems): strip pre-reduction
+// ---------------------------------------------------------------------------
+// Every atomic kernel here runs at the L2's fp64 atomic-add rate (~230e9 doubles/s, DESIGN.md
+// §5), so this shape (16 entries per element, 201 M on cfg3) has to reduce fewer doubles. A CTA
+// takes a strip of kStripElems consecutive elements of the visit order: one bulk copy brings
+// the strip's K rows (6 KB, contiguous when the K rows are consecutive; else a 128-byte copy per
+// element), one its record and one its shape (fea_plan::sk_meta / sk_shape: the shape table is
+// de-duplicated and L2-resident on regular meshes). Thread t owns the t-th distinct slot of
+// the strip: it sums the K entries that feed it from shared memory, in ascending entry order,
+// and issues ONE reduction - no shared accumulators, no barrier between elements. On a Kuhn
+// mesh a strip of 8 cubes has ~270 distinct slots for its 768 entries. Strips are handed out by
+// ticket like the hex8 patches. Conflict resolution = assemble_atomic's (atomics between strips).
+constexpr int kStripElems = 48;
+constexpr int kStripThreads = 256;
+#ifndef FEA_STRIP_STAGES
+#define FEA_STRIP_STAGES 3
+#endif
+template <int STAGES>
+__global__ void __launch_bounds__(kStripThreads)
+    k_atomic_strip(const double* __restrict__ K, const unsigned char* __restrict__ meta,
+                   const unsigned char* __restrict__ shapes, const int4* __restrict__ k0,
+                   const int32_t* __restrict__ krows, int64_t n_strip, int stride, int off_pos, int sh_stride,
+                   int off_prow, int off_ent, unsigned long long* __restrict__ ticket,
+                   double* __restrict__ values) {
+    constexpr int P = kStripElems, KB = P * 128;
+    extern __shared__ __align__(16) unsigned char smem_st[];
+    const int tid = threadIdx.x;
+    const int slot = KB + stride + sh_stride;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_st + STAGES * slot);
+    int64_t* s_q = reinterpret_cast<int64_t*>(bars + STAGES);  // 8 claimed strips, issue -> compute
+    const int64_t G = gridDim.x;
+    int64_t t_next = 0;  // thread 0: the ticket after the one being issued (round trip off the issue path)
+    auto claim = [&]() -> int64_t {
+        const int64_t r = t_next;
+        t_next = ticket ? static_cast<int64_t>(atomicAdd(ticket, 1ull)) : r + G;
+        return r;
+    };
+    auto issue = [&](int stage, int64_t st) {  // thread 0
+        const uint32_t bar = smem_u32(bars + stage);
+        if (st >= n_strip) {
+            mbar_arrive(bar);
+            return;
+        }
+        unsigned char* sb = smem_st + stage * slot;
+        fence_proxy_async_smem();  // the stage was last read by generic loads
+        const int4 kk = __ldg(k0 + st);
+        mbar_arrive_expect_tx(bar, static_cast<uint32_t>(kk.y * 128 + stride + sh_stride));
+        if (kk.x >= 0) {
+            bulk_g2s(smem_u32(sb), K + static_cast<int64_t>(kk.x) * 16, static_cast<uint32_t>(kk.y * 128), bar);
+        } else {
+            for (int k = 0; k < kk.y; ++k)
+                bulk_g2s(smem_u32(sb + k * 128), K + static_cast<int64_t>(__ldg(krows + st * P + k)) * 16, 128u, bar);
+        }
+        bulk_g2s(smem_u32(sb + KB), meta + st * stride, static_cast<uint32_t>(stride), bar);
+        bulk_g2s(smem_u32(sb + KB + stride), shapes + static_cast<int64_t>(kk.z) * sh_stride,
+                 static_cast<uint32_t>(sh_stride), bar);
+    };
+    if (tid == 0) {
+        for (int st = 0; st < STAGES; ++st) mbar_init(smem_u32(bars + st), 1);
+        mbar_fence_init();
+        t_next = ticket ? static_cast<int64_t>(atomicAdd(ticket, 1ull)) : static_cast<int64_t>(blockIdx.x);
+        for (int j = 0; j < STAGES - 1; ++j) {
+            const int64_t st = claim();
+            s_q[j & 7] = st;
+            issue(j, st);
+        }
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    for (int it = 0;; ++it) {
+        const int64_t st = s_q[it & 7];
+        if (st >= n_strip) break;  // claims only grow: every later one is past the end too
+        const int stage = it % STAGES;
+        if (tid == 0) {  // refill the stage the previous iteration released (barrier below)
+            const int j = it + STAGES - 1;
+            const int64_t sn = claim();
+            s_q[j & 7] = sn;
+            issue(j % STAGES, sn);
+        }
+        mbar_wait(smem_u32(bars + stage), (phase >> stage) & 1u);
+        phase ^= 1u << stage;
+        const unsigned char* sb = smem_st + stage * slot;
+        const unsigned char* mb = sb + KB;
+        const unsigned char* hb = mb + stride;
+        const int n_pairs = *reinterpret_cast<const int*>(mb);
+        const int64_t* rows = reinterpret_cast<const int64_t*>(mb + 16);
+        const uint8_t* ppos = mb + off_pos;
+        const uint16_t* pend = reinterpret_cast<const uint16_t*>(hb);
+        const uint8_t* prow = hb + off_prow;
+        const uint16_t* ent = reinterpret_cast<const uint16_t*>(hb + off_ent);
+        const double* Ks = reinterpret_cast<const double*>(sb);
+        for (int t = tid; t < n_pairs; t += kStripThreads) {
+            const int b = t ? pend[t - 1] : 0, e = pend[t];
+            double sum = 0.0;
+            for (int i = b; i < e; ++i) sum += Ks[ent[i]];
+            FEA_DCHECK(prow[t] < reinterpret_cast<const int*>(mb)[2] && rows[prow[t]] >= 0);
+            atomicAdd(values + rows[prow[t]] + ppos[t], sum);
+        }
+        __syncthreads();
+    }
+}
+
 // --- launch helpers --------------------------------------------------------
 
 // Per (plan, kernel, block size, shared memory): raise the kernel's dynamic shared-memory
@@ -2697,8 +2800,35 @@ void run_atomic_patch(fea_plan* p, const double* K, double* values, cudaStream_t
     p->last_launches += 1;
 }
 
+void run_atomic_strip(fea_plan* p, const double* K, double* values, cudaStream_t s) {
+    constexpr int STAGES = FEA_STRIP_STAGES;
+    const size_t smem = static_cast<size_t>(STAGES) * (kStripElems * 128 + p->sk_stride + p->sk_sh_stride) + STAGES * 8 + 64;
+    auto kern = k_atomic_strip<STAGES>;
+    const int per_sm = launch_prep(p, kern, kStripThreads, smem);
+    const int64_t blocks = std::min<int64_t>(p->sk_n, static_cast<int64_t>(p->sms) * std::max(per_sm, 1));
+    if (blocks == 0) return;
+    unsigned long long* ticket = nullptr;
+    // grid stride by default: a strip takes ~2 us, so tickets for all CTAs would be ~440 M
+    // same-address atomics per second (cfg3: 1.45 ms with tickets, 0.64 ms without)
+    if (!p->kn.patch_static && p->kn.patch_tickets) {
+        if (!p->pk_ticket.p) p->pk_ticket.alloc(kTicketRing * 8);
+        ticket = p->pk_ticket.as<unsigned long long>() + (p->pk_ticket_next++ % kTicketRing);
+        FEA_CK(cudaMemsetAsync(ticket, 0, 8, s));
+    }
+    kern<<<static_cast<unsigned>(blocks), kStripThreads, smem, s>>>(
+        K, p->sk_meta.as<unsigned char>(), p->sk_shape.as<unsigned char>(), p->sk_k0.as<int4>(),
+        p->sk_krow.as<int32_t>(), p->sk_n, p->sk_stride, p->sk_off_pos, p->sk_sh_stride, p->sk_off_prow,
+        p->sk_off_ent, ticket, values);
+    FEA_CK(cudaGetLastError());
+    p->last_launches += 1;
+}
+
 template <class PosT>
 bool atomic_staged(fea_plan* p, const double* K, double* values, cudaStream_t s) {
+    if (p->sk_n > 0 && (reinterpret_cast<uintptr_t>(K) & 15u) == 0) {  // strip pre-reduction (npe 4, d 1)
+        run_atomic_strip(p, K, values, s);
+        return true;
+    }
     if (p->pk_n > 0 && (reinterpret_cast<uintptr_t>(K) & 15u) == 0) {  // patch pre-reduction
         switch (p->d) {
             case 1: run_atomic_patch<1>(p, K, values, s); return true;

@@ -15,12 +15,16 @@
 //      FEA_COLOUR_PASSES runs it literally, one k_scatter<plain> launch per colour.
 //  FEA_ATOMIC      k_scatter<atomic>: element owner, one fp64 atomicAdd (RED.E.ADD.F64) per
 //      entry, elements in a locality order (assemble_atomic, assembly.hpp:121-126).
+#include <cstring>
+#include <unordered_map>
+
 #include "kernels.cuh"
 
 namespace feagpu {
 
 void build_atomic_maps(fea_plan* p, cudaStream_t s);
 void build_patches(fea_plan* p, cudaStream_t s);
+void build_strips(fea_plan* p, cudaStream_t s);
 
 // --- lattice-like item sequences and their tiled visit order ----------------------------------
 // Items (the patches of k_atomic_patch) in visit order. On a structured
@@ -130,6 +134,7 @@ void ensure_element_maps(fea_plan* p, cudaStream_t s) {
     }
     build_atomic_maps(p, s);
     build_patches(p, s);
+    build_strips(p, s);
 }
 
 // Patches of k_atomic_patch (npe = 8, d <= 3, byte positions, no repeated nodes): greedy growth
@@ -361,6 +366,222 @@ void build_patches(fea_plan* p, cudaStream_t s) {
     FEA_CK(cudaStreamSynchronize(s));
     p->pk_max_pairs = max_pairs;
     p->pk_n = n_patch;
+}
+
+// Strips of k_atomic_strip (npe = 4, d = 1, byte positions, no repeated nodes): kStripElems
+// consecutive elements of the atomic visit order (on a mesh whose consecutive elements share
+// nodes — the 6 Kuhn tets of a cube, a row of cubes — 768 element entries fall on ~270 distinct
+// slots). A strip's nodes are numbered by first appearance; its distinct (row node, column node)
+// pairs are sorted by those local numbers and every pair lists the strip's K entries that feed
+// it, ascending (a fixed summation order inside the strip; atomics between strips). That
+// structure — list ends, row of each pair, entry offsets: the strip's SHAPE — does not depend on
+// the node ids, so strips of a regular mesh share a handful of shapes (de-duplicated by content;
+// the kernel reads them from L2), and the per-strip record keeps only what the ids decide: the
+// values start of each row node and each pair's position in its row. Host work, once per plan
+// (first atomic assembly); both tables have fixed-size records sized by the largest strip.
+void build_strips(fea_plan* p, cudaStream_t s) {
+    if (p->npe != 4 || p->d != 1 || p->pos_bytes != 1 || p->dup_nodes || p->E == 0 || p->kn.atomic_no_patch ||
+        p->kn.atomic_no_strip || p->kn.atomic_legacy || p->sk_n > 0)
+        return;
+    constexpr int NPE = 4, NN = 16, P = kStripElems;
+    const int64_t E = p->E;
+    std::vector<int32_t> order(E), krow(E), conn(static_cast<size_t>(p->krows() * NPE));
+    std::vector<uint8_t> posE(static_cast<size_t>(E * NN));
+    std::vector<int64_t> nptr(static_cast<size_t>(p->n_own + 1));
+    FEA_CK(cudaMemcpyAsync(order.data(), p->order.p, E * 4, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaMemcpyAsync(krow.data(), p->elem_krow.p, E * 4, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaMemcpyAsync(conn.data(), p->conn_k.p, conn.size() * 4, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaMemcpyAsync(posE.data(), p->posE.p, posE.size(), cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaMemcpyAsync(nptr.data(), p->nptr.p, nptr.size() * 8, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaStreamSynchronize(s));
+    int32_t max_node = 0;
+    for (int32_t v : conn) max_node = std::max(max_node, v);
+    const int64_t nn = static_cast<int64_t>(max_node) + 1;
+    const int64_t n_strip = (E + P - 1) / P;
+    struct Strip {
+        int64_t rows_off, pairs_off;
+        int32_t n_rows, n_pairs, n_ent, n_el, shape;
+    };
+    struct Shape {
+        int64_t pairs_off, ent_off;
+        int32_t n_pairs, n_ent;
+    };
+    std::vector<Strip> st(static_cast<size_t>(n_strip));
+    std::vector<Shape> shapes;
+    std::unordered_map<uint64_t, std::vector<int32_t>> by_hash;
+    std::vector<int64_t> rows_all;                  // per strip: values start per local node (-1: not owned)
+    std::vector<uint8_t> ppos_all;                  // per strip: position of each pair in its row
+    std::vector<uint16_t> end_all, ent_all;         // per shape: list ends, entry offsets
+    std::vector<uint8_t> prow_all;                  // per shape: local row node of each pair
+    std::vector<int4> hk0(static_cast<size_t>(n_strip));
+    std::vector<int32_t> hkrow(static_cast<size_t>(n_strip * P), -1);
+    std::vector<int32_t> nstamp(nn, -1), nloc(nn, 0);
+    std::vector<int32_t> pstamp(static_cast<size_t>(P * NPE) * 256, -1);
+    std::vector<uint16_t> pidx(static_cast<size_t>(P * NPE) * 256, 0);
+    std::vector<uint8_t> kpos(static_cast<size_t>(P * NPE) * 256, 0);
+    std::vector<int32_t> keys, sorted, cnt, cnt2, ord;
+    std::vector<uint16_t> epair(P * NN), remap, newidx, t_end, t_ent;
+    std::vector<uint8_t> t_prow;
+    int max_rows = 0, max_pairs = 0, max_ent = 0;
+    const int long_len = std::getenv("FEA_STRIP_LONG") ? std::atoi(std::getenv("FEA_STRIP_LONG")) : 6;
+    for (int64_t q = 0; q < n_strip; ++q) {
+        const int n_el = static_cast<int>(std::min<int64_t>(P, E - q * P));
+        keys.clear();
+        int n_loc = 0;
+        bool contig = true;
+        const int64_t rows_off = static_cast<int64_t>(rows_all.size());
+        for (int k = 0; k < n_el; ++k) {  // local node numbers by first appearance
+            const int32_t le = order[q * P + k];
+            hkrow[q * P + k] = krow[le];
+            contig = contig && krow[le] == krow[order[q * P]] + k;
+            for (int a = 0; a < NPE; ++a) {
+                const int32_t v = conn[static_cast<size_t>(krow[le]) * NPE + a];
+                if (nstamp[v] != q) {
+                    nstamp[v] = static_cast<int32_t>(q);
+                    nloc[v] = n_loc++;
+                    const int64_t vo = static_cast<int64_t>(v) - p->node_begin;
+                    rows_all.push_back(vo >= 0 && vo < p->n_own ? nptr[vo] : -1);
+                }
+            }
+        }
+        for (int k = 0; k < n_el; ++k) {
+            const int32_t le = order[q * P + k];
+            const int32_t* cv = conn.data() + static_cast<size_t>(krow[le]) * NPE;
+            for (int a = 0; a < NPE; ++a) {
+                const int r = nloc[cv[a]];
+                const bool owned = rows_all[rows_off + r] >= 0;
+                for (int b = 0; b < NPE; ++b) {
+                    if (!owned) {  // row not owned: its entries are dropped
+                        epair[k * NN + a * NPE + b] = 0xffffu;
+                        continue;
+                    }
+                    const int key = r * 256 + nloc[cv[b]];
+                    if (pstamp[key] != q) {
+                        pstamp[key] = static_cast<int32_t>(q);
+                        pidx[key] = static_cast<uint16_t>(keys.size());
+                        kpos[key] = posE[static_cast<size_t>(le) * NN + a * NPE + b];
+                        keys.push_back(key);
+                    }
+                    epair[k * NN + a * NPE + b] = pidx[key];
+                }
+            }
+        }
+        // pairs sorted by (local row, local column); entry lists by counting sort (ascending offset)
+        sorted = keys;
+        std::sort(sorted.begin(), sorted.end());
+        remap.resize(keys.size());
+        for (size_t i = 0; i < sorted.size(); ++i) pidx[sorted[i]] = static_cast<uint16_t>(i);
+        for (size_t i = 0; i < keys.size(); ++i) remap[i] = pidx[keys[i]];
+        const int n_pairs = static_cast<int>(sorted.size());
+        cnt.assign(n_pairs + 1, 0);
+        int n_ent = 0;
+        for (int x = 0; x < n_el * NN; ++x)
+            if (epair[x] != 0xffffu) {
+                epair[x] = remap[epair[x]];
+                ++cnt[epair[x] + 1];
+                ++n_ent;
+            }
+        // thread t of the CTA sums pair t's list, and a warp runs as long as its longest list:
+        // the long lists (a node's diagonal collects an entry from each of its elements in the
+        // strip, up to 24 on a Kuhn mesh; an edge 1-6) go first, longest first, so they share
+        // warps; the short ones keep the (row, column) order, whose neighbours share sectors
+        ord.resize(n_pairs);
+        for (int i = 0; i < n_pairs; ++i) ord[i] = i;
+        std::stable_sort(ord.begin(), ord.end(), [&](int i, int j) {
+            const int li = cnt[i + 1], lj = cnt[j + 1];
+            if (long_len <= 0) return li > lj;  // FEA_STRIP_LONG=0: all by length
+            if ((li > long_len) != (lj > long_len)) return li > long_len;
+            return li > long_len ? li > lj : false;
+        });
+        newidx.resize(n_pairs);
+        for (int k = 0; k < n_pairs; ++k) newidx[ord[k]] = static_cast<uint16_t>(k);
+        cnt2.assign(n_pairs + 1, 0);
+        for (int k = 0; k < n_pairs; ++k) cnt2[k + 1] = cnt2[k] + cnt[ord[k] + 1];
+        t_end.resize(n_pairs);
+        t_prow.resize(n_pairs);
+        t_ent.resize(n_ent);
+        const int64_t pairs_off = static_cast<int64_t>(ppos_all.size());
+        for (int k = 0; k < n_pairs; ++k) {
+            t_end[k] = static_cast<uint16_t>(cnt2[k + 1]);
+            t_prow[k] = static_cast<uint8_t>(sorted[ord[k]] >> 8);
+            ppos_all.push_back(kpos[sorted[ord[k]]]);
+        }
+        for (int x = 0; x < n_el * NN; ++x)
+            if (epair[x] != 0xffffu) t_ent[cnt2[newidx[epair[x]]]++] = static_cast<uint16_t>(x);
+        // shape de-duplication by content
+        uint64_t h = 1469598103934665603ull ^ static_cast<uint64_t>(n_pairs) * 1099511628211ull;
+        auto mixin = [&](const void* d, size_t n) {
+            const unsigned char* c = static_cast<const unsigned char*>(d);
+            for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ull;
+        };
+        mixin(t_end.data(), t_end.size() * 2);
+        mixin(t_prow.data(), t_prow.size());
+        mixin(t_ent.data(), t_ent.size() * 2);
+        int32_t shape = -1;
+        for (int32_t c : by_hash[h]) {
+            const Shape& sh = shapes[c];
+            if (sh.n_pairs == n_pairs && sh.n_ent == n_ent &&
+                std::memcmp(end_all.data() + sh.pairs_off, t_end.data(), n_pairs * 2) == 0 &&
+                std::memcmp(prow_all.data() + sh.pairs_off, t_prow.data(), n_pairs) == 0 &&
+                std::memcmp(ent_all.data() + sh.ent_off, t_ent.data(), n_ent * 2) == 0) {
+                shape = c;
+                break;
+            }
+        }
+        if (shape < 0) {
+            shape = static_cast<int32_t>(shapes.size());
+            shapes.push_back({static_cast<int64_t>(end_all.size()), static_cast<int64_t>(ent_all.size()), n_pairs, n_ent});
+            end_all.insert(end_all.end(), t_end.begin(), t_end.end());
+            prow_all.insert(prow_all.end(), t_prow.begin(), t_prow.end());
+            ent_all.insert(ent_all.end(), t_ent.begin(), t_ent.end());
+            by_hash[h].push_back(shape);
+        }
+        st[q] = {rows_off, pairs_off, n_loc, n_pairs, n_ent, n_el, shape};
+        hk0[q] = make_int4(contig ? krow[order[q * P]] : -1, n_el, shape, 0);
+        max_rows = std::max(max_rows, n_loc);
+        max_pairs = std::max(max_pairs, n_pairs);
+        max_ent = std::max(max_ent, n_ent);
+    }
+    auto a16 = [](int x) { return (x + 15) & ~15; };
+    // strip record: header, row starts, pair positions; shape record: list ends, pair rows, entries
+    const int off_pos = 16 + a16(8 * max_rows), stride = off_pos + a16(std::max(max_pairs, 1));
+    const int off_prow = a16(2 * std::max(max_pairs, 1)), off_ent = off_prow + a16(std::max(max_pairs, 1)),
+              sh_stride = off_ent + a16(2 * std::max(max_ent, 1));
+    FEA_REQUIRE(static_cast<size_t>(stride) + sh_stride + P * 128 <= 64 * 1024, FEA_ERR_INVALID,
+                "internal: strip record too large");
+    std::vector<unsigned char> blob(static_cast<size_t>(n_strip) * stride, 0);
+    for (int64_t q = 0; q < n_strip; ++q) {
+        unsigned char* b = blob.data() + q * stride;
+        const int32_t hdr[4] = {st[q].n_pairs, st[q].n_ent, st[q].n_rows, st[q].n_el};
+        std::memcpy(b, hdr, 16);
+        std::memcpy(b + 16, rows_all.data() + st[q].rows_off, static_cast<size_t>(st[q].n_rows) * 8);
+        std::memcpy(b + off_pos, ppos_all.data() + st[q].pairs_off, static_cast<size_t>(st[q].n_pairs));
+    }
+    std::vector<unsigned char> sblob(shapes.size() * static_cast<size_t>(sh_stride), 0);
+    for (size_t c = 0; c < shapes.size(); ++c) {
+        unsigned char* b = sblob.data() + c * sh_stride;
+        std::memcpy(b, end_all.data() + shapes[c].pairs_off, static_cast<size_t>(shapes[c].n_pairs) * 2);
+        std::memcpy(b + off_prow, prow_all.data() + shapes[c].pairs_off, static_cast<size_t>(shapes[c].n_pairs));
+        std::memcpy(b + off_ent, ent_all.data() + shapes[c].ent_off, static_cast<size_t>(shapes[c].n_ent) * 2);
+    }
+    p->sk_meta.alloc(blob.size());
+    p->sk_shape.alloc(std::max<size_t>(sblob.size(), 16));
+    p->sk_k0.alloc(hk0.size() * 16);
+    p->sk_krow.alloc(hkrow.size() * 4);
+    FEA_CK(cudaMemcpyAsync(p->sk_meta.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
+    if (!sblob.empty()) FEA_CK(cudaMemcpyAsync(p->sk_shape.p, sblob.data(), sblob.size(), cudaMemcpyHostToDevice, s));
+    FEA_CK(cudaMemcpyAsync(p->sk_k0.p, hk0.data(), hk0.size() * 16, cudaMemcpyHostToDevice, s));
+    FEA_CK(cudaMemcpyAsync(p->sk_krow.p, hkrow.data(), hkrow.size() * 4, cudaMemcpyHostToDevice, s));
+    FEA_CK(cudaStreamSynchronize(s));
+    p->sk_stride = stride;
+    p->sk_off_pos = off_pos;
+    p->sk_sh_stride = sh_stride;
+    p->sk_off_prow = off_prow;
+    p->sk_off_ent = off_ent;
+    p->sk_n = n_strip;
+    if (std::getenv("FEA_PATCH_DEBUG"))
+        std::fprintf(stderr, "strips: n %lld shapes %zu max nodes %d pairs %d entries %d strides %d %d\n",
+                     (long long)n_strip, shapes.size(), max_rows, max_pairs, max_ent, stride, sh_stride);
 }
 
 // Visit-order metadata of k_atomic_staged (shapes d <= 3, npe in {4, 8}); other shapes, and

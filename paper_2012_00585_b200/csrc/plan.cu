@@ -69,7 +69,7 @@ Knobs read_knobs() {
     };
     return Knobs{on("FEA_ATOMIC_LEGACY"), on("FEA_ATOMIC_NO_PATCH"), on("FEA_SLOT_NO_FIXED"), on("FEA_CN_UNPACKED"),
                  on("FEA_CN_NO_RECORDS"), on("FEA_D1_NO_DIRECT"),    on("FEA_D1_NO_VEC"),
-                 on("FEA_D1_NO_LANE"),    on("FEA_PATCH_TICKETS"), on("FEA_PATCH_STATIC"), on("FEA_D1_REC8"),
+                 on("FEA_D1_NO_LANE"),    on("FEA_ATOMIC_NO_STRIP"), on("FEA_PATCH_TICKETS"), on("FEA_PATCH_STATIC"), on("FEA_D1_REC8"),
                  mod("FEA_D1_ACC_STRIDE_MOD16"), mod("FEA_D1V_ACC_STRIDE_MOD16")};
 }
 
@@ -1396,7 +1396,7 @@ int64_t metadata_bytes(const fea_plan* p) {
                                 p->ln_rec.bytes + p->ln_recC.bytes + p->cnr_hdr.bytes + p->cnr_rec.bytes +
                                 p->cnr_recC.bytes + p->slot_hdr.bytes + p->slot_rec.bytes + p->slot_recC.bytes +
                                 p->pk_hdr.bytes + p->pk_krow.bytes + p->pk_cidx.bytes + p->pk_rows.bytes + p->pk_rowpair.bytes +
-                                p->pk_pairs.bytes);
+                                p->pk_pairs.bytes + p->sk_meta.bytes + p->sk_shape.bytes + p->sk_k0.bytes + p->sk_krow.bytes);
 }
 
 }  // namespace feagpu

@@ -657,6 +657,39 @@ def test_atomic_patch_schedules(gpu, orc, env, n, perm, monkeypatch):
         assert got1.tobytes() == want1.tobytes()
 
 
+@pytest.mark.parametrize("env", [{}, {"FEA_PATCH_TICKETS": "1"}, {"FEA_STRIP_LONG": "0"}, {"FEA_ATOMIC_NO_STRIP": "1"}])
+@pytest.mark.parametrize("mesh,n,perm", [("tet4", 5, "nodes"), ("tet4", 4, "elements"), ("quad4", 13, "elements"),
+                                         ("quad4", 9, None)])
+def test_atomic_strip_paths(gpu, orc, env, mesh, n, perm, monkeypatch):
+    """k_atomic_strip (npe = 4, d = 1): consecutive K rows (one bulk copy per strip) and permuted
+    elements (a copy per element), strips by grid stride or by ticket, both pair orders, a
+    partial last strip, a row-partitioned plan, accumulate; against the sequential result within
+    the reference tolerance, bitwise with ones."""
+    import torch
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    conn, nn, ed, n_rows = problem(mesh, n, 1, perm)
+    E, m = ed.shape
+    P = orc.Pattern.build(conn, nn, 1)
+    Kh = orc.fill_k(4, E, m)
+    want = P.assemble_sequential(ed, Kh)
+    ones = np.ones_like(Kh)
+    want1 = P.assemble_sequential(ed, ones)
+    K = torch.from_numpy(Kh).cuda()
+    with gpu.Plan(ed, n_rows, dofs_per_node=1) as plan:
+        for _ in range(2):
+            assert close(plan.assemble(K, strategy="atomic").cpu().numpy(), want)
+        assert plan.assemble(torch.from_numpy(ones).cuda(), strategy="atomic").cpu().numpy().tobytes() == want1.tobytes()
+        v = torch.from_numpy(want1.copy()).cuda()  # accumulate onto existing values (exact with ones)
+        plan.assemble(torch.from_numpy(ones).cuda(), v, strategy="atomic", accumulate=True)
+        assert v.cpu().numpy().tobytes() == (2 * want1).tobytes()
+    rp, _ = P.arrays()
+    lo, hi = n_rows // 3, (2 * n_rows) // 3
+    with gpu.Plan(ed, n_rows, dofs_per_node=1, row_range=(lo, hi)) as plan:
+        got = plan.assemble(K, strategy="atomic").cpu().numpy()
+        assert close(got, want[rp[lo]:rp[hi]])
+
+
 KERNEL_SWITCHES = ["FEA_SLOT_NO_FIXED", "FEA_CN_NO_RECORDS", "FEA_D1_NO_DIRECT", "FEA_D1_NO_VEC",
                    "FEA_GATHER_NO_SLOT", "FEA_GATHER_NO_CN", "FEA_D1_NO_LANE", "FEA_D1_REC8",
                    "FEA_D1_NO_LANE,FEA_D1_NO_DIRECT"]
