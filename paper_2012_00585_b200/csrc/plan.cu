@@ -18,12 +18,16 @@
 // node b) — uint8 when every node row has <= 256 neighbour nodes — instead of
 // an int32/int64 slot per element-matrix entry.
 
+#include <chrono>
+#include <cstdio>
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "internal.cuh"
 #include "prims.cuh"
@@ -97,6 +101,21 @@ namespace {
 
 constexpr int kWarpsPerBlock = 8;
 constexpr int kNodeCap = 512;  // candidates sorted in a warp's shared-memory slice
+
+// FEA_PLAN_TRACE: per-stage wall time of the symbolic phase on stderr (synchronises the plan
+// stream at every mark; measurement only)
+struct StageTrace {
+    bool on = std::getenv("FEA_PLAN_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what, cudaStream_t s) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "plan trace: %-28s %9.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
 
 bool is_device_ptr(const void* ptr) {
     cudaPointerAttributes at{};
@@ -728,12 +747,72 @@ struct Tmp {
     }
 };
 
+// Host -> device copy of a large caller array. The reference interface hands over int64 DOFs
+// in ordinary (pageable) memory - 3.2 GB on config 5 - which a plain cudaMemcpy moves through
+// the driver's single staging thread at 5-9 GB/s (360-700 ms, five times the whole symbolic
+// phase on the device). Here a few host threads copy interleaved 8 MiB chunks into their own
+// pinned double buffers and issue the bulk transfers on their own streams, so the host-side
+// memcpy runs in parallel and overlaps the PCIe transfer. Pinned sources and small arrays take
+// the plain copy. The copy has completed when the function returns.
+void upload_host(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    constexpr size_t kChunk = size_t{8} << 20;
+    cudaPointerAttributes at{};
+    const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int T = static_cast<int>(std::min<size_t>({size_t{8}, hw > 1 ? hw / 2 : 1, bytes / (4 * kChunk)}));
+    if (pinned || T < 2 || std::getenv("FEA_PLAIN_UPLOAD")) {
+        FEA_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        FEA_CK(cudaStreamSynchronize(s));
+        return;
+    }
+    int dev = 0;
+    FEA_CK(cudaGetDevice(&dev));
+    const size_t n_chunks = (bytes + kChunk - 1) / kChunk;
+    std::vector<cudaError_t> err(static_cast<size_t>(T), cudaSuccess);
+    auto worker = [&](int t) {
+        cudaError_t& e = err[static_cast<size_t>(t)];
+        auto ok = [&](cudaError_t r) {
+            if (e == cudaSuccess && r != cudaSuccess) e = r;
+            return e == cudaSuccess;
+        };
+        unsigned char* stage[2] = {nullptr, nullptr};
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        cudaStream_t st = nullptr;
+        if (ok(cudaSetDevice(dev)) && ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking))) {
+            for (int b = 0; b < 2; ++b) {
+                ok(cudaHostAlloc(reinterpret_cast<void**>(&stage[b]), kChunk, cudaHostAllocDefault));
+                ok(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+            }
+            int b = 0;
+            for (size_t c = static_cast<size_t>(t); c < n_chunks && e == cudaSuccess; c += static_cast<size_t>(T), b ^= 1) {
+                const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+                if (!ok(cudaEventSynchronize(ev[b]))) break;  // the buffer's previous transfer
+                std::memcpy(stage[b], static_cast<const unsigned char*>(src) + off, len);
+                ok(cudaMemcpyAsync(static_cast<unsigned char*>(dst) + off, stage[b], len, cudaMemcpyHostToDevice, st));
+                ok(cudaEventRecord(ev[b], st));
+            }
+            ok(cudaStreamSynchronize(st));
+        }
+        for (int b = 0; b < 2; ++b) {
+            if (ev[b]) cudaEventDestroy(ev[b]);
+            if (stage[b]) cudaFreeHost(stage[b]);
+        }
+        if (st) cudaStreamDestroy(st);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < T; ++t) pool.emplace_back(worker, t);
+    worker(0);
+    for (std::thread& th : pool) th.join();
+    for (cudaError_t e : err) FEA_CK(e);
+}
+
 // Upload (or alias) the element DOF array.
 const int64_t* device_dofs(const int64_t* elem_dofs, int64_t n, DevBuf& hold, cudaStream_t s) {
     if (n == 0) return nullptr;
     if (is_device_ptr(elem_dofs)) return elem_dofs;
     hold.alloc(n * sizeof(int64_t));
-    FEA_CK(cudaMemcpyAsync(hold.p, elem_dofs, n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    upload_host(hold.p, elem_dofs, n * sizeof(int64_t), s);
     return hold.as<int64_t>();
 }
 
@@ -1133,6 +1212,7 @@ void build_runs(fea_plan* p, cudaStream_t s) {
 }
 
 void build_own_pattern(fea_plan* p, cudaStream_t s) {
+    StageTrace tr;
     const unsigned blocks = grid_for(p->n_own * 32, kWarpsPerBlock * 32);
     DevBuf counts, big, nbig, maxbig;
     counts.alloc((p->n_own + 1) * sizeof(int64_t));
@@ -1168,7 +1248,9 @@ void build_own_pattern(fea_plan* p, cudaStream_t s) {
             big.as<int32_t>(), counts.as<int64_t>(), nullptr, nullptr);
         FEA_CK(cudaGetLastError());
     }
+    tr.mark("node pattern (count)", s);
     finish_counts(p, counts, s);
+    tr.mark("row pointer scan", s);
     p->ncol.alloc(p->nnz_nodes * 4);
     if (p->n_own > 0)
         k_node_pattern<true><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
@@ -1180,6 +1262,7 @@ void build_own_pattern(fea_plan* p, cudaStream_t s) {
             p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
             big.as<int32_t>(), nullptr, p->nptr.as<int64_t>(), p->ncol.as<int32_t>());
     FEA_CK(cudaGetLastError());
+    tr.mark("node pattern (fill)", s);
     // slot map (adjacency order)
     p->posA.alloc(p->n_adj * p->pstride * p->pos_bytes + 64);
     FEA_CK(cudaMemsetAsync(p->posA.p, 0, p->posA.bytes, s));
@@ -1194,9 +1277,13 @@ void build_own_pattern(fea_plan* p, cudaStream_t s) {
                 p->n_own, p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->pstride, p->posA.as<uint16_t>());
         FEA_CK(cudaGetLastError());
     }
+    tr.mark("slot map", s);
     build_runs(p, s);
+    tr.mark("CRAC runs", s);
     build_node_order(p, s);
+    tr.mark("node order", s);
     build_traversal(p, s);
+    tr.mark("traversal records", s);
 }
 
 // Common front end: DOFs -> node connectivity (with node-layout detection),
@@ -1438,8 +1525,11 @@ fea_status fea_plan_create(int device, const int64_t* elem_dofs, int64_t n_eleme
         p->row_begin = row_begin;
         p->row_end = row_end;
         p->k_compact = (flags & FEA_PLAN_K_COMPACT) != 0;
+        StageTrace tr;
         build_elements(p.get(), elem_dofs, dofs_per_node, st.s);
+        tr.mark("DOFs -> connectivity", st.s);
         build_adjacency(p.get(), st.s);
+        tr.mark("incidences sort + scan", st.s);
         build_own_pattern(p.get(), st.s);
         FEA_CK(cudaStreamSynchronize(st.s));
         *out = p.release();
