@@ -18,6 +18,8 @@
 #include <cstring>
 #include <unordered_map>
 
+#include <chrono>
+
 #include "kernels.cuh"
 
 namespace feagpu {
@@ -137,6 +139,175 @@ void ensure_element_maps(fea_plan* p, cudaStream_t s) {
     build_strips(p, s);
 }
 
+// --- patch tables on the device -----------------------------------------------------------------
+// One warp per patch (P = 8 element slots of npe = 8 nodes): the patch's owned row nodes, sorted
+// and made unique (row index = rank of the node id), and its distinct (row, position) pairs, keys
+// row << 8 | position, sorted and made unique - warp bitonic sorts in shared memory like the
+// symbolic phase's k_node_pattern. FILL = false counts rows and pairs per patch; after the two
+// exclusive scans FILL = true writes the header, the row words, the row pair ranges, the pair
+// list, the K row of every element slot and the pair index of every (slot, a, b).
+constexpr int kPtWarps = 4;
+__device__ __forceinline__ void patch_bitonic(int32_t* s, int n, int lane) {  // n: power of two
+    for (int k = 2; k <= n; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < n; i += 32) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const int32_t a = s[i], b = s[ixj];
+                    if ((a > b) == ((i & k) == 0)) {
+                        s[i] = b;
+                        s[ixj] = a;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+}
+// compact the distinct values of sorted s[0..n) (INT32_MAX = none) to its front; returns the count
+__device__ __forceinline__ int patch_unique(int32_t* s, int n, int lane) {
+    int total = 0;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+        const int i = i0 + lane;
+        const int32_t x = s[i];
+        const bool uniq = x != INT32_MAX && (i == 0 || x != s[i - 1]);
+        const unsigned bal = __ballot_sync(0xffffffffu, uniq);
+        __syncwarp();  // every lane has read s[i] and s[i - 1] of this step
+        if (uniq) s[total + __popc(bal & ((1u << lane) - 1u))] = x;  // total + rank <= i: no later step reads it
+        total += __popc(bal);
+        __syncwarp();
+    }
+    return total;
+}
+__device__ __forceinline__ int patch_find(const int32_t* s, int n, int32_t x) {  // x is present
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+template <bool FILL>
+__global__ void __launch_bounds__(kPtWarps * 32)
+    k_patch_tables(const int32_t* __restrict__ members, int64_t n_patch, const int32_t* __restrict__ elem_krow,
+                   const int32_t* __restrict__ conn_k, const uint8_t* __restrict__ posE,
+                   const int64_t* __restrict__ nptr, int64_t node_begin, int64_t n_own, int d,
+                   int64_t* __restrict__ n_rows_out, int64_t* __restrict__ n_pairs_out,
+                   const int64_t* __restrict__ row_off, const int64_t* __restrict__ pair_off, int max_pairs,
+                   int4* __restrict__ hdr, int32_t* __restrict__ pk_krow, uint16_t* __restrict__ pk_cidx,
+                   int64_t* __restrict__ pk_rows, int32_t* __restrict__ pk_rowpair, uint16_t* __restrict__ pk_pairs) {
+    constexpr int P = kPatchElems, NPE = 8, NN = 64;
+    __shared__ int32_t s_node[kPtWarps][P * NPE];
+    __shared__ int32_t s_key[kPtWarps][P * NN];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int32_t* rows = s_node[w];
+    int32_t* keys = s_key[w];
+    for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < n_patch;
+         q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        // the patch's (slot, a) nodes: 64 entries, two per lane
+        int32_t le[2], nd[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int x = lane + 32 * h, k = x / NPE, a = x - k * NPE;
+            le[h] = members[q * P + k];
+            nd[h] = INT32_MAX;
+            if (le[h] >= 0) {
+                const int32_t v = conn_k[static_cast<int64_t>(elem_krow[le[h]]) * NPE + a];
+                if (v >= node_begin && v - node_begin < n_own) nd[h] = v;
+            }
+            rows[x] = nd[h];
+        }
+        __syncwarp();
+        patch_bitonic(rows, P * NPE, lane);
+        const int n_rows = patch_unique(rows, P * NPE, lane);
+        // pair keys: row << 8 | position of every entry (slot, a, b) with an owned row node
+        for (int x = lane; x < P * NN; x += 32) keys[x] = INT32_MAX;
+        __syncwarp();
+        int r[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            r[h] = nd[h] != INT32_MAX ? patch_find(rows, n_rows, nd[h]) : -1;
+            if (r[h] >= 0) {
+                const int x = lane + 32 * h;
+                const uint2 pz = *reinterpret_cast<const uint2*>(posE + static_cast<int64_t>(le[h]) * NN + (x % NPE) * NPE);
+#pragma unroll
+                for (int b = 0; b < NPE; ++b)
+                    keys[x * NPE + b] = (r[h] << 8) | static_cast<int>(((b < 4 ? pz.x : pz.y) >> (8 * (b & 3))) & 0xffu);
+            }
+        }
+        __syncwarp();
+        patch_bitonic(keys, P * NN, lane);
+        const int n_pairs = patch_unique(keys, P * NN, lane);
+        if (!FILL) {
+            if (lane == 0) {
+                n_rows_out[q] = n_rows;
+                n_pairs_out[q] = n_pairs;
+            }
+        } else {
+            const int64_t ro = row_off[q], po = pair_off[q];
+            int n_el = 0;
+            for (int k = 0; k < P; ++k) n_el += members[q * P + k] >= 0;
+            if (lane == 0)
+                hdr[q] = make_int4(0, static_cast<int>(po), static_cast<int>(ro), n_el | (n_rows << 8) | (n_pairs << 16));
+            if (lane < P) {
+                const int32_t e = members[q * P + lane];
+                pk_krow[q * P + lane] = e >= 0 ? elem_krow[e] : -1;
+            }
+            for (int i = lane; i < n_rows; i += 32) {
+                const int64_t vo = rows[i] - node_begin, c0 = nptr[vo];
+                pk_rows[ro + i] = ((static_cast<int64_t>(d) * d * c0) << 20) | (static_cast<int64_t>(d) * (nptr[vo + 1] - c0));
+                // pairs are sorted by row: the row's range is [first key >= i << 8, first key >= (i + 1) << 8)
+                int lo = 0, hi = n_pairs;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (keys[mid] < (i << 8)) lo = mid + 1;
+                    else hi = mid;
+                }
+                int lo2 = lo, hi2 = n_pairs;
+                while (lo2 < hi2) {
+                    const int mid = (lo2 + hi2) >> 1;
+                    if (keys[mid] < ((i + 1) << 8)) lo2 = mid + 1;
+                    else hi2 = mid;
+                }
+                pk_rowpair[ro + i] = lo | ((lo2 - lo) << 16);
+            }
+            for (int i = lane; i < n_pairs; i += 32) pk_pairs[po + i] = static_cast<uint16_t>(keys[i]);
+            // pair index of every entry; a row node outside the owned range -> the spare pair
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (le[h] < 0) continue;
+                const int x = lane + 32 * h;
+                uint16_t* out = pk_cidx + (q * P + x / NPE) * NN + (x % NPE) * NPE;
+                const uint2 pz = *reinterpret_cast<const uint2*>(posE + static_cast<int64_t>(le[h]) * NN + (x % NPE) * NPE);
+#pragma unroll
+                for (int b = 0; b < NPE; ++b) {
+                    const int pos = static_cast<int>(((b < 4 ? pz.x : pz.y) >> (8 * (b & 3))) & 0xffu);
+                    out[b] = r[h] >= 0 ? static_cast<uint16_t>(patch_find(keys, n_pairs, (r[h] << 8) | pos))
+                                       : static_cast<uint16_t>(max_pairs);
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void k_max2_i64(const int64_t* __restrict__ a, const int64_t* __restrict__ b, int64_t n,
+                           unsigned long long* out) {  // out[0] = max a, out[1] = max b
+    unsigned long long ma = 0, mb = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        ma = max(ma, static_cast<unsigned long long>(a[i]));
+        mb = max(mb, static_cast<unsigned long long>(b[i]));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        ma = max(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+        mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(out, ma);
+        atomicMax(out + 1, mb);
+    }
+}
+
 // Patches of k_atomic_patch (npe = 8, d <= 3, byte positions, no repeated nodes): greedy growth
 // from the atomic visit order — the first unassigned element, then repeatedly the unassigned
 // element sharing the most nodes with the patch (ties: earlier in the visit order) — up to
@@ -149,14 +320,19 @@ void build_patches(fea_plan* p, cudaStream_t s) {
         return;
     constexpr int NPE = 8, NN = 64, P = kPatchElems;
     const int64_t E = p->E;
+    const bool trace = std::getenv("FEA_PLAN_TRACE") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "patch trace: %-28s %9.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     std::vector<int32_t> order(E), krow(E), conn(static_cast<size_t>(p->krows() * NPE));
-    std::vector<uint8_t> posE(static_cast<size_t>(E * NN));
-    std::vector<int64_t> nptr(static_cast<size_t>(p->n_own + 1));
     FEA_CK(cudaMemcpyAsync(order.data(), p->order.p, E * 4, cudaMemcpyDeviceToHost, s));
     FEA_CK(cudaMemcpyAsync(krow.data(), p->elem_krow.p, E * 4, cudaMemcpyDeviceToHost, s));
     FEA_CK(cudaMemcpyAsync(conn.data(), p->conn_k.p, conn.size() * 4, cudaMemcpyDeviceToHost, s));
-    FEA_CK(cudaMemcpyAsync(posE.data(), p->posE.p, posE.size(), cudaMemcpyDeviceToHost, s));
-    FEA_CK(cudaMemcpyAsync(nptr.data(), p->nptr.p, nptr.size() * 8, cudaMemcpyDeviceToHost, s));
     FEA_CK(cudaStreamSynchronize(s));
     auto node = [&](int64_t le, int a) { return conn[static_cast<size_t>(krow[le]) * NPE + a]; };
     int32_t max_node = 0;
@@ -176,6 +352,7 @@ void build_patches(fea_plan* p, cudaStream_t s) {
     }
     std::vector<int32_t> vpos(E);
     for (int64_t i = 0; i < E; ++i) vpos[order[i]] = static_cast<int32_t>(i);
+    mark("copies + node->element index");
     // greedy patches
     std::vector<char> assigned(E, 0);
     std::vector<int32_t> stamp(E, -1);
@@ -220,6 +397,7 @@ void build_patches(fea_plan* p, cudaStream_t s) {
         ++pid;
     }
     const int64_t n_patch = pid;
+    mark("greedy growth");
     // Tiled visit order for lattice-like patch sequences (a structured mesh in lexicographic
     // order: patch q shares nodes with q + 1, q + s1 +- 1, q + s2 +- s1 +- 1). In sequence order
     // the patches of the next plane come s2 patches later (config 5: 16,384 patches = 0.6 GB of
@@ -266,104 +444,54 @@ void build_patches(fea_plan* p, cudaStream_t s) {
             members.swap(m2);
         }
     }
-    // per patch: rows, pairs, element pair indices
-    std::vector<int32_t> hk(static_cast<size_t>(n_patch * P), -1);
-    std::vector<uint16_t> hc(static_cast<size_t>(n_patch * P * NN), 0xffffu);
-    std::vector<int4> hh(static_cast<size_t>(n_patch));
-    std::vector<int64_t> hrows;
-    std::vector<int32_t> hrowpair;
-    std::vector<uint16_t> hpairs;
-    hrows.reserve(static_cast<size_t>(n_patch) * 30);
-    hpairs.reserve(static_cast<size_t>(n_patch) * 350);
-    std::vector<int32_t> nstamp(nn, -1), nrow(nn, 0);
-    std::vector<int32_t> pstamp(64 * 256, -1);
-    std::vector<uint16_t> pidx(64 * 256, 0);
-    int max_pairs = 0;
-    for (int64_t q = 0; q < n_patch; ++q) {
-        int n_rows = 0, n_el = 0;
-        std::vector<int64_t> prow;   // row node (owned, local) per row index
-        std::vector<int32_t> keys;   // row << 8 | pos per pair (insertion order)
-        uint16_t tmp[P][NN];
-        for (int k = 0; k < P; ++k) {
-            const int32_t le = members[q * P + k];
-            for (int x = 0; x < NN; ++x) tmp[k][x] = 0xffffu;
-            if (le < 0) continue;
-            ++n_el;
-            hk[q * P + k] = krow[le];
-            for (int a = 0; a < NPE; ++a) {
-                const int64_t vo = static_cast<int64_t>(node(le, a)) - p->node_begin;
-                if (vo < 0 || vo >= p->n_own) continue;
-                const int32_t v = node(le, a);
-                if (nstamp[v] != q) {
-                    nstamp[v] = static_cast<int32_t>(q);
-                    nrow[v] = n_rows++;
-                    prow.push_back(vo);
-                }
-                const int r = nrow[v];
-                for (int b = 0; b < NPE; ++b) {
-                    const int key = r * 256 + posE[static_cast<size_t>(le) * NN + a * NPE + b];
-                    if (pstamp[key] != q) {
-                        pstamp[key] = static_cast<int32_t>(q);
-                        pidx[key] = static_cast<uint16_t>(keys.size());
-                        keys.push_back(key);
-                    }
-                    tmp[k][a * NPE + b] = pidx[key];
-                }
-            }
-        }
-        // sort pairs by (row, position); remap the element indices
-        std::vector<int32_t> sorted(keys);
-        std::sort(sorted.begin(), sorted.end());
-        std::vector<uint16_t> remap(keys.size());
-        for (size_t i2 = 0; i2 < sorted.size(); ++i2) pidx[sorted[i2]] = static_cast<uint16_t>(i2);
-        for (size_t i2 = 0; i2 < keys.size(); ++i2) remap[i2] = pidx[keys[i2]];
-        for (int k = 0; k < P; ++k)
-            for (int x = 0; x < NN; ++x)
-                if (tmp[k][x] != 0xffffu) hc[(q * P + k) * NN + x] = remap[tmp[k][x]];
-        FEA_REQUIRE(hpairs.size() + sorted.size() < (size_t{1} << 31) && n_rows < 256, FEA_ERR_INVALID,
-                    "internal: patch tables too large");
-        hh[q] = make_int4(0, static_cast<int>(hpairs.size()), static_cast<int>(hrows.size()),
-                          n_el | (n_rows << 8) | (static_cast<int>(sorted.size()) << 16));
-        for (int64_t vo : prow) {
-            const int64_t c0 = nptr[vo];
-            hrows.push_back(((static_cast<int64_t>(p->d) * p->d * c0) << 20) |
-                            (static_cast<int64_t>(p->d) * (nptr[vo + 1] - c0)));
-        }
-        {  // first pair and pair count per row (pairs sorted by row index)
-            std::vector<int32_t> first(prow.size(), 0), count(prow.size(), 0);
-            for (size_t i2 = 0; i2 < sorted.size(); ++i2) {
-                const int r = sorted[i2] >> 8;
-                if (count[r]++ == 0) first[r] = static_cast<int32_t>(i2);
-            }
-            for (size_t r = 0; r < prow.size(); ++r) hrowpair.push_back(first[r] | (count[r] << 16));
-        }
-        for (int32_t key : sorted) hpairs.push_back(static_cast<uint16_t>(((key >> 8) << 8) | (key & 0xff)));
-        max_pairs = std::max<int>(max_pairs, static_cast<int>(sorted.size()));
-    }
-    // entries of a row node outside the owned range add into the spare pair (index max_pairs,
-    // allocated by the kernel and never flushed): no branch per entry in the kernel
-    for (int64_t q = 0; q < n_patch; ++q) {
-        const int n_el = hh[q].w & 0xff;
-        for (int k = 0; k < n_el; ++k)
-            for (int x = 0; x < NN; ++x) {
-                uint16_t& c = hc[(q * P + k) * NN + x];
-                if (c == 0xffffu) c = static_cast<uint16_t>(max_pairs);
-            }
-    }
-    p->pk_hdr.alloc(std::max<int64_t>(n_patch, 1) * 16);
-    p->pk_krow.alloc(hk.size() * 4);
-    p->pk_cidx.alloc(hc.size() * 2);
-    p->pk_rows.alloc(std::max<size_t>(hrows.size(), 1) * 8);
-    p->pk_pairs.alloc(std::max<size_t>(hpairs.size(), 1) * 2);
-    p->pk_rowpair.alloc(std::max<size_t>(hrowpair.size(), 1) * 4);
-    if (!hrowpair.empty())
-        FEA_CK(cudaMemcpyAsync(p->pk_rowpair.p, hrowpair.data(), hrowpair.size() * 4, cudaMemcpyHostToDevice, s));
-    FEA_CK(cudaMemcpyAsync(p->pk_hdr.p, hh.data(), hh.size() * 16, cudaMemcpyHostToDevice, s));
-    FEA_CK(cudaMemcpyAsync(p->pk_krow.p, hk.data(), hk.size() * 4, cudaMemcpyHostToDevice, s));
-    FEA_CK(cudaMemcpyAsync(p->pk_cidx.p, hc.data(), hc.size() * 2, cudaMemcpyHostToDevice, s));
-    if (!hrows.empty()) FEA_CK(cudaMemcpyAsync(p->pk_rows.p, hrows.data(), hrows.size() * 8, cudaMemcpyHostToDevice, s));
-    if (!hpairs.empty()) FEA_CK(cudaMemcpyAsync(p->pk_pairs.p, hpairs.data(), hpairs.size() * 2, cudaMemcpyHostToDevice, s));
+    mark("lattice + tiles");
+    // per patch: rows, pairs, element pair indices - on the device (k_patch_tables): a count pass,
+    // two exclusive scans for the row and pair offsets, a fill pass
+    DevBuf d_mem, d_nr, d_np, d_ro, d_po, d_mx;
+    d_mem.alloc(members.size() * 4);
+    FEA_CK(cudaMemcpyAsync(d_mem.p, members.data(), members.size() * 4, cudaMemcpyHostToDevice, s));
+    d_nr.alloc((n_patch + 1) * 8);
+    d_np.alloc((n_patch + 1) * 8);
+    d_ro.alloc((n_patch + 1) * 8);
+    d_po.alloc((n_patch + 1) * 8);
+    d_mx.alloc(16);
+    FEA_CK(cudaMemsetAsync(d_nr.p, 0, d_nr.bytes, s));
+    FEA_CK(cudaMemsetAsync(d_np.p, 0, d_np.bytes, s));
+    FEA_CK(cudaMemsetAsync(d_mx.p, 0, 16, s));
+    const unsigned pt_blocks = grid_for(n_patch * 32, kPtWarps * 32);
+    k_patch_tables<false><<<pt_blocks, kPtWarps * 32, 0, s>>>(
+        d_mem.as<int32_t>(), n_patch, p->elem_krow.as<int32_t>(), p->conn_k.as<int32_t>(), p->posE.as<uint8_t>(),
+        p->nptr.as<int64_t>(), p->node_begin, p->n_own, p->d, d_nr.as<int64_t>(), d_np.as<int64_t>(), nullptr, nullptr,
+        0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    FEA_CK(cudaGetLastError());
+    k_max2_i64<<<grid_for(n_patch, 256), 256, 0, s>>>(d_nr.as<int64_t>(), d_np.as<int64_t>(), n_patch,
+                                                      d_mx.as<unsigned long long>());
+    exclusive_sum(d_nr.as<int64_t>(), d_ro.as<int64_t>(), n_patch + 1, s);
+    exclusive_sum(d_np.as<int64_t>(), d_po.as<int64_t>(), n_patch + 1, s);
+    unsigned long long h_mx[2] = {0, 0};
+    int64_t tot_rows = 0, tot_pairs = 0;
+    FEA_CK(cudaMemcpyAsync(h_mx, d_mx.p, 16, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaMemcpyAsync(&tot_rows, d_ro.as<int64_t>() + n_patch, 8, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaMemcpyAsync(&tot_pairs, d_po.as<int64_t>() + n_patch, 8, cudaMemcpyDeviceToHost, s));
     FEA_CK(cudaStreamSynchronize(s));
+    FEA_REQUIRE(tot_pairs < (int64_t{1} << 31) && tot_rows < (int64_t{1} << 31), FEA_ERR_INVALID,
+                "internal: patch tables too large");
+    const int max_pairs = static_cast<int>(h_mx[1]);
+    p->pk_hdr.alloc(std::max<int64_t>(n_patch, 1) * 16);
+    p->pk_krow.alloc(static_cast<size_t>(n_patch) * P * 4);
+    p->pk_cidx.alloc(static_cast<size_t>(n_patch) * P * NN * 2);
+    p->pk_rows.alloc(std::max<int64_t>(tot_rows, 1) * 8);
+    p->pk_pairs.alloc(std::max<int64_t>(tot_pairs, 1) * 2);
+    p->pk_rowpair.alloc(std::max<int64_t>(tot_rows, 1) * 4);
+    FEA_CK(cudaMemsetAsync(p->pk_cidx.p, 0xff, p->pk_cidx.bytes, s));
+    k_patch_tables<true><<<pt_blocks, kPtWarps * 32, 0, s>>>(
+        d_mem.as<int32_t>(), n_patch, p->elem_krow.as<int32_t>(), p->conn_k.as<int32_t>(), p->posE.as<uint8_t>(),
+        p->nptr.as<int64_t>(), p->node_begin, p->n_own, p->d, nullptr, nullptr, d_ro.as<int64_t>(), d_po.as<int64_t>(),
+        max_pairs, p->pk_hdr.as<int4>(), p->pk_krow.as<int32_t>(), p->pk_cidx.as<uint16_t>(), p->pk_rows.as<int64_t>(),
+        p->pk_rowpair.as<int32_t>(), p->pk_pairs.as<uint16_t>());
+    FEA_CK(cudaGetLastError());
+    FEA_CK(cudaStreamSynchronize(s));
+    mark("patch tables (device)");
     p->pk_max_pairs = max_pairs;
     p->pk_n = n_patch;
 }

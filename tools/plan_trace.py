@@ -27,6 +27,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--lazy", action="store_true", help="time the first call of each route (lazily built tables)")
     a = ap.parse_args()
     kind, n, perm, d = CONFIGS[a.config]
     conn, nn = M.make_mesh(kind, n, perm)
@@ -42,6 +43,23 @@ def main():
             torch.cuda.synchronize()
             ms = (time.perf_counter() - t0) * 1e3
             print(f"cfg{a.config} DOFs on {where} rep {rep}: plan {ms:.1f} ms, nnz {plan.nnz}", file=sys.stderr, flush=True)
+            if a.lazy and where == "device" and rep == 0:
+                K = fea.fill_seeded_k(conn.shape[0], ed.shape[1], 42)
+                v = torch.zeros(plan.nnz, dtype=torch.float64, device="cuda")
+                for strategy in ("sorted", "atomic", "atomic"):
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    plan.assemble(K, v, strategy=strategy, accumulate=strategy == "atomic")
+                    torch.cuda.synchronize()
+                    print(f"cfg{a.config} {strategy} call: {(time.perf_counter() - t0) * 1e3:.1f} ms", file=sys.stderr, flush=True)
+                t0 = time.perf_counter()
+                col, nc = plan.greedy_colouring()
+                t1 = time.perf_counter()
+                plan.set_colouring(col)
+                torch.cuda.synchronize()
+                print(f"cfg{a.config} greedy colouring {(t1 - t0) * 1e3:.1f} ms ({nc} colours), set_colouring "
+                      f"{(time.perf_counter() - t1) * 1e3:.1f} ms", file=sys.stderr, flush=True)
+                del K, v
             plan.close()
         del src
 
