@@ -313,7 +313,9 @@ __global__ void k_max2_i64(const int64_t* __restrict__ a, const int64_t* __restr
 // element sharing the most nodes with the patch (ties: earlier in the visit order) — up to
 // kPatchElems elements; on structured hex8 meshes this tiles 2 x 2 x 2 blocks. Per patch the
 // distinct (owned row node, column node) pairs, sorted by (row, position), and per element the
-// pair index of each (a, b). Host work, once per plan (on the first atomic assembly).
+// pair index of each (a, b). Once per plan, on the first atomic assembly: the greedy growth (a
+// sequential sweep) and the lattice order run on the host, the tables are built on the device
+// (k_patch_tables; 12 s of a 16 s first call on config 5 when they were built on one host thread).
 void build_patches(fea_plan* p, cudaStream_t s) {
     if (p->npe != 8 || p->d > 3 || p->pos_bytes != 1 || p->dup_nodes || p->E == 0 || p->kn.atomic_no_patch ||
         p->kn.atomic_legacy || p->pk_n > 0)

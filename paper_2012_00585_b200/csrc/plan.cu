@@ -315,6 +315,83 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     }
 }
 
+// One pass instead of three (count, fill, slot map) for the common case - no high-valence node,
+// rows of <= 256 column nodes (byte positions): the sorted unique list of a node is written to a
+// scratch array at the node's candidate offset adj_ptr[v] * npe (an upper bound of its length,
+// disjoint between nodes), its length to counts[v], and the node's slot-map rows posA straight
+// from the list in shared memory (positions are row-relative, so they need no row pointer).
+// After the row-pointer scan k_compact_lists copies the lists to ncol + nptr[v]. The caller
+// falls back to the separate passes when a node was deferred or a row is longer than 256.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_node_pattern_fused(const int64_t* __restrict__ adj_ptr, const int32_t* __restrict__ adj,
+                         const int32_t* __restrict__ conn_k, int npe, int64_t n_own, int64_t* __restrict__ counts,
+                         int32_t* __restrict__ scratch, int pstride, uint8_t* __restrict__ posA,
+                         int32_t* __restrict__ big_list, unsigned* __restrict__ n_big,
+                         unsigned* __restrict__ max_big) {
+    __shared__ int32_t sh[kWarpsPerBlock][kNodeCap];
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    int32_t* s = sh[w];
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n_own;
+         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t b0 = adj_ptr[v];
+        const int64_t nc = (adj_ptr[v + 1] - b0) * npe;
+        if (nc > kNodeCap) {
+            if (lane == 0) {
+                big_list[atomicAdd(n_big, 1u)] = static_cast<int32_t>(v);
+                atomicMax(max_big, static_cast<unsigned>(nc));
+            }
+            continue;
+        }
+        int P = 1;
+        while (P < nc) P <<= 1;
+        for (int i = lane; i < P; i += 32)
+            s[i] = i < nc ? candidate(adj, conn_k, b0, npe, i) : INT32_MAX;
+        __syncwarp();
+        warp_bitonic(s, P, lane);
+        int total = 0;  // distinct values compacted to the front of s (a slot is never written
+                        // before the step that reads it: total + rank <= i)
+        for (int i0 = 0; i0 < P; i0 += 32) {
+            const int i = i0 + lane;
+            const int32_t x = i < P ? s[i] : INT32_MAX;  // (P may be smaller than a warp)
+            const bool uniq = x != INT32_MAX && (i == 0 || x != s[i - 1]);
+            const unsigned bal = __ballot_sync(0xffffffffu, uniq);
+            __syncwarp();
+            if (uniq) s[total + __popc(bal & ((1u << lane) - 1u))] = x;
+            total += __popc(bal);
+            __syncwarp();
+        }
+        if (lane == 0) counts[v] = total;
+        int32_t* out = scratch + b0 * npe;
+        for (int i = lane; i < total; i += 32) out[i] = s[i];
+        if (total <= 256)
+            for (int i = lane; i < nc; i += 32) {
+                const int32_t u = candidate(adj, conn_k, b0, npe, i);
+                int lo = 0, hi = total;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s[mid] < u) lo = mid + 1;
+                    else hi = mid;
+                }
+                const int k = i / npe;
+                posA[(b0 + k) * pstride + (i - k * npe)] = static_cast<uint8_t>(lo);
+            }
+        __syncwarp();
+    }
+}
+
+__global__ void k_compact_lists(const int64_t* __restrict__ adj_ptr, const int32_t* __restrict__ scratch, int npe,
+                                int64_t n_own, const int64_t* __restrict__ nptr, int32_t* __restrict__ ncol) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n_own;
+         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t c0 = nptr[v];
+        const int cnt = static_cast<int>(nptr[v + 1] - c0);
+        const int32_t* src = scratch + adj_ptr[v] * npe;
+        for (int i = lane; i < cnt; i += 32) ncol[c0 + i] = src[i];
+    }
+}
+
 // Block-per-node fallback for high-valence nodes (dynamic shared memory).
 template <bool FILL>
 __global__ void k_node_pattern_big(const int64_t* __restrict__ adj_ptr,
@@ -1214,7 +1291,7 @@ void build_runs(fea_plan* p, cudaStream_t s) {
 void build_own_pattern(fea_plan* p, cudaStream_t s) {
     StageTrace tr;
     const unsigned blocks = grid_for(p->n_own * 32, kWarpsPerBlock * 32);
-    DevBuf counts, big, nbig, maxbig;
+    DevBuf counts, big, nbig, maxbig, scratch;
     counts.alloc((p->n_own + 1) * sizeof(int64_t));
     FEA_CK(cudaMemsetAsync(counts.p, 0, counts.bytes, s));
     big.alloc((p->n_own + 1) * 4);
@@ -1222,11 +1299,26 @@ void build_own_pattern(fea_plan* p, cudaStream_t s) {
     maxbig.alloc(4);
     FEA_CK(cudaMemsetAsync(nbig.p, 0, 4, s));
     FEA_CK(cudaMemsetAsync(maxbig.p, 0, 4, s));
-    if (p->n_own > 0)
-        k_node_pattern<false><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
-            p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
-            p->n_own, counts.as<int64_t>(), nullptr, nullptr, big.as<int32_t>(),
-            nbig.as<unsigned>(), maxbig.as<unsigned>());
+    // fused pass (k_node_pattern_fused): lists to scratch, byte positions to posA
+    const bool try_fused = std::getenv("FEA_PLAN_NO_FUSED") == nullptr;
+    const int pstride1 = (p->npe + 3) / 4 * 4;
+    if (try_fused) {
+        scratch.alloc(std::max<int64_t>(p->n_adj * p->npe, 1) * 4);
+        p->posA.alloc(p->n_adj * pstride1 + 64);
+        FEA_CK(cudaMemsetAsync(p->posA.p, 0, p->posA.bytes, s));
+    }
+    if (p->n_own > 0) {
+        if (try_fused)
+            k_node_pattern_fused<<<blocks, kWarpsPerBlock * 32, 0, s>>>(
+                p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe, p->n_own,
+                counts.as<int64_t>(), scratch.as<int32_t>(), pstride1, p->posA.as<uint8_t>(), big.as<int32_t>(),
+                nbig.as<unsigned>(), maxbig.as<unsigned>());
+        else
+            k_node_pattern<false><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
+                p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
+                p->n_own, counts.as<int64_t>(), nullptr, nullptr, big.as<int32_t>(),
+                nbig.as<unsigned>(), maxbig.as<unsigned>());
+    }
     FEA_CK(cudaGetLastError());
     unsigned h_nbig = 0, h_maxbig = 0;
     FEA_CK(cudaMemcpyAsync(&h_nbig, nbig.p, 4, cudaMemcpyDeviceToHost, s));
@@ -1248,35 +1340,46 @@ void build_own_pattern(fea_plan* p, cudaStream_t s) {
             big.as<int32_t>(), counts.as<int64_t>(), nullptr, nullptr);
         FEA_CK(cudaGetLastError());
     }
-    tr.mark("node pattern (count)", s);
+    tr.mark(try_fused ? "node pattern (fused)" : "node pattern (count)", s);
     finish_counts(p, counts, s);
     tr.mark("row pointer scan", s);
     p->ncol.alloc(p->nnz_nodes * 4);
-    if (p->n_own > 0)
-        k_node_pattern<true><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
-            p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
-            p->n_own, nullptr, p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), big.as<int32_t>(),
-            nbig.as<unsigned>(), maxbig.as<unsigned>());
-    if (h_nbig > 0)
-        k_node_pattern_big<true><<<h_nbig, 256, big_smem, s>>>(
-            p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
-            big.as<int32_t>(), nullptr, p->nptr.as<int64_t>(), p->ncol.as<int32_t>());
-    FEA_CK(cudaGetLastError());
-    tr.mark("node pattern (fill)", s);
-    // slot map (adjacency order)
-    p->posA.alloc(p->n_adj * p->pstride * p->pos_bytes + 64);
-    FEA_CK(cudaMemsetAsync(p->posA.p, 0, p->posA.bytes, s));
-    if (p->n_own > 0) {
-        if (p->pos_bytes == 1)
-            k_pos_adj<uint8_t><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
-                p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
-                p->n_own, p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->pstride, p->posA.as<uint8_t>());
-        else
-            k_pos_adj<uint16_t><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
-                p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
-                p->n_own, p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->pstride, p->posA.as<uint16_t>());
+    const bool fused = try_fused && h_nbig == 0 && p->pos_bytes == 1;
+    if (fused) {
+        if (p->n_own > 0)
+            k_compact_lists<<<blocks, kWarpsPerBlock * 32, 0, s>>>(p->adj_ptr.as<int64_t>(), scratch.as<int32_t>(),
+                                                                   p->npe, p->n_own, p->nptr.as<int64_t>(),
+                                                                   p->ncol.as<int32_t>());
         FEA_CK(cudaGetLastError());
+        tr.mark("list compaction", s);
+    } else {
+        if (p->n_own > 0)
+            k_node_pattern<true><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
+                p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
+                p->n_own, nullptr, p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), big.as<int32_t>(),
+                nbig.as<unsigned>(), maxbig.as<unsigned>());
+        if (h_nbig > 0)
+            k_node_pattern_big<true><<<h_nbig, 256, big_smem, s>>>(
+                p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
+                big.as<int32_t>(), nullptr, p->nptr.as<int64_t>(), p->ncol.as<int32_t>());
+        FEA_CK(cudaGetLastError());
+        tr.mark("node pattern (fill)", s);
+        // slot map (adjacency order)
+        p->posA.alloc(p->n_adj * p->pstride * p->pos_bytes + 64);
+        FEA_CK(cudaMemsetAsync(p->posA.p, 0, p->posA.bytes, s));
+        if (p->n_own > 0) {
+            if (p->pos_bytes == 1)
+                k_pos_adj<uint8_t><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
+                    p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
+                    p->n_own, p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->pstride, p->posA.as<uint8_t>());
+            else
+                k_pos_adj<uint16_t><<<blocks, kWarpsPerBlock * 32, 0, s>>>(
+                    p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(), p->conn_k.as<int32_t>(), p->npe,
+                    p->n_own, p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), p->pstride, p->posA.as<uint16_t>());
+            FEA_CK(cudaGetLastError());
+        }
     }
+    scratch.reset();
     tr.mark("slot map", s);
     build_runs(p, s);
     tr.mark("CRAC runs", s);
