@@ -64,6 +64,7 @@ struct Knobs {
     bool atomic_no_strip;  // FEA_ATOMIC_NO_STRIP: k_atomic_staged instead of strip pre-reduction (npe 4, d 1)
     bool patch_tickets;  // FEA_PATCH_TICKETS: tickets also for short runs
     bool patch_static;  // FEA_PATCH_STATIC: k_atomic_patch CTAs stride by the grid size instead of taking tickets
+    bool gather_global;  // FEA_GATHER_GLOBAL: k_gather_global (accumulate in the values array) for every plan
     bool d1_rec8;  // FEA_D1_REC8: 8-byte lane records even where the compact 4-byte form fits
     int d1_acc_mod, d1v_acc_mod;  // accumulator stride residues (mod 16 doubles)
 };
@@ -193,6 +194,7 @@ struct fea_plan {
     // bookkeeping
     feagpu::Knobs kn = {};     // A/B switches as the environment had them when the plan was created
     int32_t last_launches = 0;
+    bool gather_global = false;  // no shared-memory gather fits the largest row block: k_gather_global
     bool gen_on = false;       // fea_assemble_seeded in progress: kernels generate K
     uint64_t gen_seed = 0;
     bool cn_disabled = false;  // FEA_GATHER_NO_CN=1: decode-table gather (A/B)

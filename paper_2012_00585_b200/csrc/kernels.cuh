@@ -71,6 +71,15 @@ __device__ __forceinline__ double kval(uint64_t seed, int64_t e, int i, int j) {
 
 // Fused supplier: when on, the gather kernels generate K[e][i][j] in registers instead of
 // reading it (fea_assemble_seeded) — no 8*E*m^2 bytes of K traffic.
+// Thrown by a gather launcher whose shared-memory layout cannot hold the plan's largest node
+// row block (a hub node with hundreds of neighbours, or d * m > 512): gather() then takes
+// k_gather_global, which accumulates in the values array itself.
+struct DoesNotFit {};
+#define FEA_FITS(cond)                  \
+    do {                                \
+        if (!(cond)) throw DoesNotFit{}; \
+    } while (0)
+
 struct GenK {
     int on;
     uint64_t seed;
@@ -2311,12 +2320,10 @@ void run_gather_stream(fea_plan* p, const Incidences& in, const double* K, doubl
     const int acc_stride = p->d * p->d * p->max_cnt + 1;  // +1 staggers groups across banks
     constexpr int kBlk = blk_of<G>();
     const int pw_blk = kBlk * p->pstride * static_cast<int>(sizeof(PosT)) / 4;
-    FEA_REQUIRE((pw_blk + G - 1) / G <= kPosW, FEA_ERR_INVALID,
-                "position map of one element too large for the gather kernel's staging");
+    FEA_FITS((pw_blk + G - 1) / G <= kPosW);
     const size_t smem = static_cast<size_t>(kWarps) * GPW *
                         (acc_stride * sizeof(double) + 2 * (kBlk + pw_blk) * sizeof(int32_t));
-    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID,
-                "node row block too large for shared-memory accumulation");
+    FEA_FITS(smem <= 227 * 1024);
     auto kern = p->dup_nodes ? k_gather_stream<G, R, PF, PosT, false> : k_gather_stream<G, R, PF, PosT, true>;
     const int occ = launch_prep(p, kern, kWarps * 32, smem);
     const int n_sm = p->sms;
@@ -2341,8 +2348,7 @@ void run_gather_node(fea_plan* p, const Incidences& in, const double* K, double*
     const int pos_stride = static_cast<int>((std::max<int64_t>(p->max_adj, 1) * p->pstride + 7) & ~int64_t(7));
     size_t smem = static_cast<size_t>(kWarps) * GPW *
                   (acc_stride * sizeof(double) + pos_stride * sizeof(PosT));
-    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID,
-                "node row block too large for shared-memory accumulation");
+    FEA_FITS(smem <= 227 * 1024);
     auto kern = p->gen_on ? (p->dup_nodes ? k_gather_node<G, R, PF, PosT, false, true>
                                           : k_gather_node<G, R, PF, PosT, true, true>)
                           : (p->dup_nodes ? k_gather_node<G, R, PF, PosT, false, false>
@@ -2484,7 +2490,7 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
     const int64_t cta_acc = cn_cta_acc(p, kWarps * GPW, s);
     const size_t smem = static_cast<size_t>(cta_acc) * sizeof(double) +
                         static_cast<size_t>(kWarps) * GPW * pos_stride * sizeof(PosT);
-    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
+    FEA_FITS(smem <= 227 * 1024);
     if (G == 32 && sizeof(PosT) == 1 && !p->dup_nodes && p->max_adj <= kCnrSlots &&
         p->npe <= kCnrBytes - 4 && (in.adj == p->adj.as<int32_t>() || in.adj == p->adjC.as<int32_t>()) &&
         !p->kn.cn_no_records &&
@@ -2503,7 +2509,7 @@ void run_gather_cn(fea_plan* p, const Incidences& in, const double* K, double* v
             }
         }
         const size_t smem_r = static_cast<size_t>(cta_acc) * sizeof(double) + kWarps * kCnrSlots * kCnrBytes;
-        FEA_REQUIRE(smem_r <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
+        FEA_FITS(smem_r <= 227 * 1024);
         auto kr = p->gen_on ? k_gather_cnr<D, FEA_CNR_PF, true> : k_gather_cnr<D, FEA_CNR_PF, false>;
         launch_prep(p, kr, kWarps * 32, smem_r);
         if (p->win_query) {
@@ -2558,7 +2564,7 @@ void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* v
     if (((rec_stride / 2) & 1) == 0) rec_stride += 2;
     const size_t smem = static_cast<size_t>(kWarps) * GPW *
                         (acc_stride * sizeof(double) + static_cast<size_t>(rec_stride) * sizeof(int32_t));
-    FEA_REQUIRE(smem <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
+    FEA_FITS(smem <= 227 * 1024);
     auto kern = p->gen_on ? (p->dup_nodes ? k_gather_d1<G, PF, PosT, false, true> : k_gather_d1<G, PF, PosT, true, true>)
                           : (p->dup_nodes ? k_gather_d1<G, PF, PosT, false, false> : k_gather_d1<G, PF, PosT, true, false>);
     const int64_t per_cta = static_cast<int64_t>(kWarps) * GPW;
@@ -2623,7 +2629,7 @@ void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* v
         while ((acc_stride2 & 15) != acc_mod2) ++acc_stride2;
         const size_t smem2 = static_cast<size_t>(kWarps) * GPW2 *
                              (acc_stride2 * sizeof(double) + static_cast<size_t>(rec_stride) * sizeof(int32_t));
-        FEA_REQUIRE(smem2 <= 227 * 1024, FEA_ERR_INVALID, "node row block too large for shared-memory accumulation");
+        FEA_FITS(smem2 <= 227 * 1024);
 #ifndef FEA_D1V_PF
 #define FEA_D1V_PF 4
 #endif
@@ -2650,9 +2656,86 @@ void run_gather_d1(fea_plan* p, const Incidences& in, const double* K, double* v
     p->last_launches += 1;
 }
 
+// Deterministic routes without a shared-memory accumulator, for plans whose largest node row
+// block fits none of the kernels above: a warp owns a node and folds the node's incident row
+// blocks, in incidence order, straight into the node's block of the values array (nobody else
+// writes it; __syncwarp orders the lanes' reads and writes between incidences). Without repeated
+// nodes the entries of one incidence hit distinct slots and are spread over the lanes; with
+// repeated nodes the columns go one after the other, as scatter_element's loop does. Per slot a
+// left fold from the start value in incidence order: the bits of the kernels above.
+template <class PosT>
+__global__ void __launch_bounds__(256)
+    k_gather_global(const double* __restrict__ K, const int64_t* __restrict__ adj_ptr, const int32_t* __restrict__ adj,
+                    const PosT* __restrict__ posA, const int64_t* __restrict__ nptr, int64_t n_own, int d, int npe,
+                    int pstride, int accumulate, int dup_nodes, GenK gen, double* values) {
+    const int lane = threadIdx.x & 31;
+    const int dd = d * d, m = d * npe;
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n_own;
+         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t b0 = adj_ptr[v], c0 = nptr[v];
+        const int n = static_cast<int>(adj_ptr[v + 1] - b0);
+        const int64_t rowlen = static_cast<int64_t>(d) * (nptr[v + 1] - c0);
+        double* blk = values + static_cast<int64_t>(dd) * c0;
+        if (!accumulate)
+            for (int64_t i = lane; i < d * rowlen; i += 32) blk[i] = 0.0;
+        __syncwarp();
+        for (int k = 0; k < n; ++k) {
+            const int32_t entry = adj[b0 + k];
+            const int64_t krow = entry / npe;
+            const int a = static_cast<int>(entry - krow * npe);
+            const double* src = K + static_cast<int64_t>(entry) * d * m;
+            const uint64_t he = gen.on ? kgen_elem(gen.seed, gen.ids ? gen.ids[krow] : krow) : 0;
+            const PosT* pos = posA + (b0 + k) * pstride;
+            auto add = [&](int b, int t) {
+                const int ki = t / d, kj = t - ki * d;
+                const double x = gen.on ? kgen_entry(he, a * d + ki, b * d + kj) : src[ki * m + b * d + kj];
+                double* dst = blk + ki * rowlen + static_cast<int64_t>(pos[b]) * d + kj;
+                *dst += x;
+            };
+            if (!dup_nodes) {
+                for (int t = lane; t < npe * dd; t += 32) add(t / dd, t % dd);
+                __syncwarp();
+            } else {
+                for (int b = 0; b < npe; ++b) {
+                    for (int t = lane; t < dd; t += 32) add(b, t);
+                    __syncwarp();
+                }
+            }
+        }
+    }
+}
+
+template <class PosT>
+void run_gather_global(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
+                       cudaStream_t s) {
+    if (no_window(p) || p->n_own == 0) return;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((p->n_own + 7) / 8, static_cast<int64_t>(p->sms) * 8));
+    k_gather_global<PosT><<<blocks, 256, 0, s>>>(K, p->adj_ptr.as<int64_t>(), in.adj, static_cast<const PosT*>(in.posA),
+                                                 p->nptr.as<int64_t>(), p->n_own, p->d, p->npe, p->pstride,
+                                                 accumulate ? 1 : 0, p->dup_nodes ? 1 : 0, gen_of(p), values);
+    FEA_CK(cudaGetLastError());
+    p->last_launches += 1;
+}
+
+template <class PosT>
+void gather_fitting(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate, cudaStream_t s);
+
 template <class PosT>
 void gather(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
             cudaStream_t s) {
+    if (!p->gather_global && !p->kn.gather_global) {
+        try {
+            return gather_fitting<PosT>(p, in, K, values, accumulate, s);
+        } catch (const DoesNotFit&) {
+            p->gather_global = true;  // the checks precede every launch: nothing has run yet
+        }
+    }
+    run_gather_global<PosT>(p, in, K, values, accumulate, s);
+}
+
+template <class PosT>
+void gather_fitting(fea_plan* p, const Incidences& in, const double* K, double* values, bool accumulate,
+                    cudaStream_t s) {
     const int dm = p->d * p->m;
     // lane = column node (d in {2,3,4}, npe <= 32); measured faster than the decode-table
     // kernels for every such shape
@@ -2703,7 +2786,7 @@ void gather(fea_plan* p, const Incidences& in, const double* K, double* values, 
     else if (dm <= 128) run_gather<32, 4, 2, PosT>(p, in, K, values, accumulate, s);
     else if (dm <= 256) run_gather<32, 8, 2, PosT>(p, in, K, values, accumulate, s);
     else if (dm <= 512) run_gather<32, 16, 1, PosT>(p, in, K, values, accumulate, s);
-    else throw Error(FEA_ERR_INVALID, "element row block (d*m) larger than 512 entries");
+    else throw DoesNotFit{};
 }
 
 template <int G, class PosT, bool ATOMIC>

@@ -16,6 +16,8 @@
 //  FEA_ATOMIC      k_scatter<atomic>: element owner, one fp64 atomicAdd (RED.E.ADD.F64) per
 //      entry, elements in a locality order (assemble_atomic, assembly.hpp:121-126).
 #include <cstring>
+#include <exception>
+#include <thread>
 #include <unordered_map>
 
 #include <chrono>
@@ -140,10 +142,10 @@ void ensure_element_maps(fea_plan* p, cudaStream_t s) {
 }
 
 // --- patch tables on the device -----------------------------------------------------------------
-// One warp per patch (P = 8 element slots of npe = 8 nodes): the patch's owned row nodes, sorted
-// and made unique (row index = rank of the node id), and its distinct (row, position) pairs, keys
-// row << 8 | position, sorted and made unique - warp bitonic sorts in shared memory like the
-// symbolic phase's k_node_pattern. FILL = false counts rows and pairs per patch; after the two
+// One warp per patch (P = 8 element slots of npe = 8 nodes): the patch's owned row nodes in order
+// of first appearance, and its distinct (row, position) pairs, keys row << 8 | position, sorted
+// and made unique - a warp bitonic sort in shared memory like the symbolic phase's
+// k_node_pattern. FILL = false counts rows and pairs per patch; after the two
 // exclusive scans FILL = true writes the header, the row words, the row pair ranges, the pair
 // list, the K row of every element slot and the pair index of every (slot, a, b).
 constexpr int kPtWarps = 4;
@@ -198,9 +200,11 @@ __global__ void __launch_bounds__(kPtWarps * 32)
                    int64_t* __restrict__ pk_rows, int32_t* __restrict__ pk_rowpair, uint16_t* __restrict__ pk_pairs) {
     constexpr int P = kPatchElems, NPE = 8, NN = 64;
     __shared__ int32_t s_node[kPtWarps][P * NPE];
+    __shared__ int32_t s_cand[kPtWarps][P * NPE];
     __shared__ int32_t s_key[kPtWarps][P * NN];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int32_t* rows = s_node[w];
+    int32_t* cand = s_cand[w];
     int32_t* keys = s_key[w];
     for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < n_patch;
          q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -215,18 +219,41 @@ __global__ void __launch_bounds__(kPtWarps * 32)
                 const int32_t v = conn_k[static_cast<int64_t>(elem_krow[le[h]]) * NPE + a];
                 if (v >= node_begin && v - node_begin < n_own) nd[h] = v;
             }
-            rows[x] = nd[h];
+            cand[x] = nd[h];
         }
         __syncwarp();
-        patch_bitonic(rows, P * NPE, lane);
-        const int n_rows = patch_unique(rows, P * NPE, lane);
-        // pair keys: row << 8 | position of every entry (slot, a, b) with an owned row node
-        for (int x = lane; x < P * NN; x += 32) keys[x] = INT32_MAX;
-        __syncwarp();
+        // rows in order of first appearance over (slot, a) - the order the flush walks them in
+        // (sorted by node id measured 2 % slower on cfg2 and config 5): an entry is a row's first
+        // when no earlier entry names its node; its row index is the number of firsts before it
+        int fx[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int x = lane + 32 * h;
+            fx[h] = x;
+            if (nd[h] != INT32_MAX)
+                for (int y = 0; y < x; ++y)
+                    if (cand[y] == nd[h]) {
+                        fx[h] = y;
+                        break;
+                    }
+        }
+        const unsigned f0 = __ballot_sync(0xffffffffu, nd[0] != INT32_MAX && fx[0] == lane);
+        const unsigned f1 = __ballot_sync(0xffffffffu, nd[1] != INT32_MAX && fx[1] == lane + 32);
+        auto rank_of = [&](int y) {
+            return y < 32 ? __popc(f0 & ((1u << y) - 1u)) : __popc(f0) + __popc(f1 & ((1u << (y - 32)) - 1u));
+        };
+        const int n_rows = __popc(f0) + __popc(f1);
         int r[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            r[h] = nd[h] != INT32_MAX ? patch_find(rows, n_rows, nd[h]) : -1;
+            r[h] = nd[h] != INT32_MAX ? rank_of(fx[h]) : -1;
+            if (r[h] >= 0 && fx[h] == lane + 32 * h) rows[r[h]] = nd[h];
+        }
+        // pair keys: row << 8 | position of every entry (slot, a, b) with an owned row node
+        for (int x = lane; x < P * NN; x += 32) keys[x] = INT32_MAX;
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
             if (r[h] >= 0) {
                 const int x = lane + 32 * h;
                 const uint2 pz = *reinterpret_cast<const uint2*>(posE + static_cast<int64_t>(le[h]) * NN + (x % NPE) * NPE);
@@ -537,14 +564,29 @@ void build_strips(fea_plan* p, cudaStream_t s) {
         int32_t n_pairs, n_ent;
     };
     std::vector<Strip> st(static_cast<size_t>(n_strip));
-    std::vector<Shape> shapes;
-    std::unordered_map<uint64_t, std::vector<int32_t>> by_hash;
-    std::vector<int64_t> rows_all;                  // per strip: values start per local node (-1: not owned)
-    std::vector<uint8_t> ppos_all;                  // per strip: position of each pair in its row
-    std::vector<uint16_t> end_all, ent_all;         // per shape: list ends, entry offsets
-    std::vector<uint8_t> prow_all;                  // per shape: local row node of each pair
     std::vector<int4> hk0(static_cast<size_t>(n_strip));
     std::vector<int32_t> hkrow(static_cast<size_t>(n_strip * P), -1);
+    const int long_len = std::getenv("FEA_STRIP_LONG") ? std::atoi(std::getenv("FEA_STRIP_LONG")) : 6;
+    // The strips are independent: host threads take contiguous ranges of them, each with its own
+    // scratch arrays, outputs and shape table (offsets and shape ids local to the range); the
+    // ranges are then concatenated in order and their shapes de-duplicated against each other,
+    // so the result does not depend on the number of threads.
+    struct Part {
+        std::vector<Shape> shapes;
+        std::vector<int64_t> rows_all;           // per strip: values start per local node (-1: not owned)
+        std::vector<uint8_t> ppos_all;           // per strip: position of each pair in its row
+        std::vector<uint16_t> end_all, ent_all;  // per shape: list ends, entry offsets
+        std::vector<uint8_t> prow_all;           // per shape: local row node of each pair
+        int max_rows = 0, max_pairs = 0, max_ent = 0;
+    };
+    auto work = [&](int64_t q_begin, int64_t q_end, Part& part) {
+    std::vector<Shape>& shapes = part.shapes;
+    std::unordered_map<uint64_t, std::vector<int32_t>> by_hash;
+    std::vector<int64_t>& rows_all = part.rows_all;
+    std::vector<uint8_t>& ppos_all = part.ppos_all;
+    std::vector<uint16_t>&end_all = part.end_all, &ent_all = part.ent_all;
+    std::vector<uint8_t>& prow_all = part.prow_all;
+    int &max_rows = part.max_rows, &max_pairs = part.max_pairs, &max_ent = part.max_ent;
     std::vector<int32_t> nstamp(nn, -1), nloc(nn, 0);
     std::vector<int32_t> pstamp(static_cast<size_t>(P * NPE) * 256, -1);
     std::vector<uint16_t> pidx(static_cast<size_t>(P * NPE) * 256, 0);
@@ -552,9 +594,7 @@ void build_strips(fea_plan* p, cudaStream_t s) {
     std::vector<int32_t> keys, sorted, cnt, cnt2, ord;
     std::vector<uint16_t> epair(P * NN), remap, newidx, t_end, t_ent;
     std::vector<uint8_t> t_prow;
-    int max_rows = 0, max_pairs = 0, max_ent = 0;
-    const int long_len = std::getenv("FEA_STRIP_LONG") ? std::atoi(std::getenv("FEA_STRIP_LONG")) : 6;
-    for (int64_t q = 0; q < n_strip; ++q) {
+    for (int64_t q = q_begin; q < q_end; ++q) {
         const int n_el = static_cast<int>(std::min<int64_t>(P, E - q * P));
         keys.clear();
         int n_loc = 0;
@@ -671,6 +711,69 @@ void build_strips(fea_plan* p, cudaStream_t s) {
         max_rows = std::max(max_rows, n_loc);
         max_pairs = std::max(max_pairs, n_pairs);
         max_ent = std::max(max_ent, n_ent);
+    }
+    };
+    const int n_thr = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>({int64_t{16}, static_cast<int64_t>(std::thread::hardware_concurrency()), n_strip / 1024})));
+    std::vector<Part> parts(static_cast<size_t>(n_thr));
+    std::vector<int64_t> cut(static_cast<size_t>(n_thr) + 1);
+    for (int t = 0; t <= n_thr; ++t) cut[t] = n_strip * t / n_thr;
+    {
+        std::vector<std::thread> pool;
+        std::vector<std::exception_ptr> errs(static_cast<size_t>(n_thr));
+        auto run = [&](int t) {
+            try {
+                work(cut[t], cut[t + 1], parts[t]);
+            } catch (...) {
+                errs[t] = std::current_exception();
+            }
+        };
+        for (int t = 1; t < n_thr; ++t) pool.emplace_back(run, t);
+        run(0);
+        for (std::thread& th : pool) th.join();
+        for (const std::exception_ptr& e : errs)
+            if (e) std::rethrow_exception(e);
+    }
+    // concatenate the ranges; shapes de-duplicated by content across ranges
+    std::vector<Shape> shapes;
+    std::vector<int64_t> rows_all;
+    std::vector<uint8_t> ppos_all, prow_all;
+    std::vector<uint16_t> end_all, ent_all;
+    int max_rows = 0, max_pairs = 0, max_ent = 0;
+    for (int t = 0; t < n_thr; ++t) {
+        Part& pt = parts[t];
+        std::vector<int32_t> map(pt.shapes.size());
+        for (size_t c = 0; c < pt.shapes.size(); ++c) {
+            const Shape& sh = pt.shapes[c];
+            int32_t g = -1;
+            for (size_t k = 0; k < shapes.size() && g < 0; ++k)
+                if (shapes[k].n_pairs == sh.n_pairs && shapes[k].n_ent == sh.n_ent &&
+                    std::memcmp(end_all.data() + shapes[k].pairs_off, pt.end_all.data() + sh.pairs_off, sh.n_pairs * 2) == 0 &&
+                    std::memcmp(prow_all.data() + shapes[k].pairs_off, pt.prow_all.data() + sh.pairs_off, sh.n_pairs) == 0 &&
+                    std::memcmp(ent_all.data() + shapes[k].ent_off, pt.ent_all.data() + sh.ent_off, sh.n_ent * 2) == 0)
+                    g = static_cast<int32_t>(k);
+            if (g < 0) {
+                g = static_cast<int32_t>(shapes.size());
+                shapes.push_back({static_cast<int64_t>(end_all.size()), static_cast<int64_t>(ent_all.size()), sh.n_pairs, sh.n_ent});
+                end_all.insert(end_all.end(), pt.end_all.begin() + sh.pairs_off, pt.end_all.begin() + sh.pairs_off + sh.n_pairs);
+                prow_all.insert(prow_all.end(), pt.prow_all.begin() + sh.pairs_off, pt.prow_all.begin() + sh.pairs_off + sh.n_pairs);
+                ent_all.insert(ent_all.end(), pt.ent_all.begin() + sh.ent_off, pt.ent_all.begin() + sh.ent_off + sh.n_ent);
+            }
+            map[c] = g;
+        }
+        const int64_t rows_base = static_cast<int64_t>(rows_all.size()), pairs_base = static_cast<int64_t>(ppos_all.size());
+        for (int64_t q = cut[t]; q < cut[t + 1]; ++q) {
+            st[q].rows_off += rows_base;
+            st[q].pairs_off += pairs_base;
+            st[q].shape = map[st[q].shape];
+            hk0[q].z = st[q].shape;
+        }
+        rows_all.insert(rows_all.end(), pt.rows_all.begin(), pt.rows_all.end());
+        ppos_all.insert(ppos_all.end(), pt.ppos_all.begin(), pt.ppos_all.end());
+        max_rows = std::max(max_rows, pt.max_rows);
+        max_pairs = std::max(max_pairs, pt.max_pairs);
+        max_ent = std::max(max_ent, pt.max_ent);
+        pt = Part{};
     }
     auto a16 = [](int x) { return (x + 15) & ~15; };
     // strip record: header, row starts, pair positions; shape record: list ends, pair rows, entries

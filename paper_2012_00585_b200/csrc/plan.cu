@@ -73,7 +73,7 @@ Knobs read_knobs() {
     };
     return Knobs{on("FEA_ATOMIC_LEGACY"), on("FEA_ATOMIC_NO_PATCH"), on("FEA_SLOT_NO_FIXED"), on("FEA_CN_UNPACKED"),
                  on("FEA_CN_NO_RECORDS"), on("FEA_D1_NO_DIRECT"),    on("FEA_D1_NO_VEC"),
-                 on("FEA_D1_NO_LANE"),    on("FEA_ATOMIC_NO_STRIP"), on("FEA_PATCH_TICKETS"), on("FEA_PATCH_STATIC"), on("FEA_D1_REC8"),
+                 on("FEA_D1_NO_LANE"),    on("FEA_ATOMIC_NO_STRIP"), on("FEA_PATCH_TICKETS"), on("FEA_PATCH_STATIC"), on("FEA_GATHER_GLOBAL"), on("FEA_D1_REC8"),
                  mod("FEA_D1_ACC_STRIDE_MOD16"), mod("FEA_D1V_ACC_STRIDE_MOD16")};
 }
 

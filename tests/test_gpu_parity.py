@@ -482,6 +482,99 @@ def test_degenerate_elements_all_strategies(gpu, orc, mesh, n, d, perm):
         assert close(plan.assemble(K, strategy="atomic").cpu().numpy(), want)
 
 
+def _hub_mesh(kind):
+    """Quads around a hub node: 'wide' - 200 quads, each with 3 nodes of its own (the hub has 800
+    candidate nodes and a row of 601 columns: block-per-node pattern kernel, 2-byte positions);
+    'dense' - 140 quads drawn from a ring of 40 nodes (560 candidates, a row of 41 columns:
+    block-per-node kernel with byte positions)."""
+    if kind == "wide":
+        conn = np.array([[0, 3 * i + 1, 3 * i + 2, 3 * i + 3] for i in range(200)], np.int64)
+        return conn, 601
+    ring = 40
+    conn = np.array([[0, 1 + i % ring, 1 + (i * 7 + 3) % ring, 1 + (i * 11 + 5) % ring] for i in range(140)], np.int64)
+    return conn, ring + 1
+
+
+@pytest.mark.parametrize("env", [{}, {"FEA_PLAN_NO_FUSED": "1"}])
+@pytest.mark.parametrize("kind,d", [("wide", 1), ("wide", 2), ("dense", 1), ("dense", 3)])
+def test_high_valence_hub(gpu, orc, kind, d, env, monkeypatch):
+    """A node with more than 512 candidate column nodes takes the block-per-node pattern kernel
+    (k_node_pattern_big), and the fused symbolic pass hands over to the separate count / fill /
+    slot-map passes; pattern, CRAC arrays and every strategy against the oracle."""
+    import torch
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    conn, nn = _hub_mesh(kind)
+    ed = M.element_dofs(conn, d)
+    P = orc.Pattern.build(conn, nn, d)
+    Kh = orc.fill_k(21, conn.shape[0], ed.shape[1])
+    want = P.assemble_sequential(ed, Kh)
+    col, _ = orc.greedy_colouring(conn, nn)
+    want_col = P.assemble_coloured(ed, Kh, col)
+    K = torch.from_numpy(Kh).cuda()
+    with gpu.Plan(ed, nn * d, dofs_per_node=d) as plan:
+        rp, cs = plan.csr()
+        orp, ocs = P.arrays()
+        assert np.array_equal(rp, orp) and np.array_equal(cs, ocs)
+        crp, cal = plan.crac()
+        ocrp, ocal = P.crac()
+        assert np.array_equal(crp, ocrp) and np.array_equal(cal, ocal)
+        assert plan.assemble(K, strategy="sorted").cpu().numpy().tobytes() == want.tobytes()
+        plan.set_colouring(col)
+        assert plan.assemble(K, strategy="colour").cpu().numpy().tobytes() == want_col.tobytes()
+        assert close(plan.assemble(K, strategy="atomic").cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("mesh,n,d,perm,env", [("hex27", 2, 7, None, {}), ("hex8", 3, 3, "elements", {"FEA_GATHER_GLOBAL": "1"}),
+                                               ("quad4", 5, 2, "nodes", {"FEA_GATHER_GLOBAL": "1"})])
+def test_global_gather_fallback(gpu, orc, mesh, n, d, perm, env, monkeypatch):
+    """k_gather_global (accumulation in the values array, for plans whose largest row block fits no
+    shared-memory gather: here hex27 with d = 7, d * m = 1,323 entries per row block, and forced on
+    common shapes): sorted, colour, fused supplier and accumulate bit-exact, repeated nodes too."""
+    import torch
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    conn, nn = M.make_mesh(mesh, n, perm)
+    for collapse in (False, True):
+        c2 = M.collapse_elements(conn, np.random.default_rng(5)) if collapse else conn
+        ed = M.element_dofs(c2, d)
+        P = orc.Pattern.build(c2, nn, d)
+        Kh = orc.fill_k(3, c2.shape[0], ed.shape[1])
+        want = P.assemble_sequential(ed, Kh)
+        col, _ = orc.greedy_colouring(c2, nn)
+        K = torch.from_numpy(Kh).cuda()
+        with gpu.Plan(ed, nn * d, dofs_per_node=d) as plan:
+            assert plan.assemble(K, strategy="sorted").cpu().numpy().tobytes() == want.tobytes()
+            assert plan.assemble_seeded(3, strategy="sorted").cpu().numpy().tobytes() == want.tobytes()
+            v = torch.from_numpy(want.copy()).cuda()
+            plan.assemble(K, v, strategy="sorted", accumulate=True)
+            assert v.cpu().numpy().tobytes() == P.assemble_sequential(ed, Kh, want.copy()).tobytes()
+            plan.set_colouring(col)
+            assert plan.assemble(K, strategy="colour").cpu().numpy().tobytes() == P.assemble_coloured(ed, Kh, col).tobytes()
+            assert close(plan.assemble(K, strategy="atomic").cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("env", [{"FEA_PLAN_NO_FUSED": "1"}])
+@pytest.mark.parametrize("mesh,n,d,perm", [("hex8", 4, 3, "elements"), ("tet4", 4, 1, "nodes"), ("hex27", 2, 3, None),
+                                           ("quad4", 9, 2, None)])
+def test_three_pass_symbolic_route(gpu, orc, mesh, n, d, perm, env, monkeypatch):
+    """The separate count / fill / slot-map passes (the route of rows longer than 256 columns and
+    of high-valence nodes) give the same pattern and values as the fused pass."""
+    import torch
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    conn, nn, ed, n_rows = problem(mesh, n, d, perm)
+    P = orc.Pattern.build(conn, nn, d)
+    Kh = orc.fill_k(8, conn.shape[0], ed.shape[1])
+    with gpu.Plan(ed, n_rows, dofs_per_node=d) as plan:
+        rp, cs = plan.csr()
+        orp, ocs = P.arrays()
+        assert np.array_equal(rp, orp) and np.array_equal(cs, ocs)
+        got = plan.assemble(torch.from_numpy(Kh).cuda(), strategy="sorted").cpu().numpy()
+        assert got.tobytes() == P.assemble_sequential(ed, Kh).tobytes()
+        assert close(plan.assemble(torch.from_numpy(Kh).cuda(), strategy="atomic").cpu().numpy(), got)
+
+
 @pytest.mark.parametrize("mesh,n,d", [("hex8", 3, 3), ("tet4", 2, 2), ("quad4", 4, 2)])
 def test_isolated_rows_and_unaligned_k(gpu, orc, mesh, n, d):
     """Rows of nodes no element touches (their CSR rows are empty), and an element-matrix buffer
@@ -692,7 +785,7 @@ def test_atomic_strip_paths(gpu, orc, env, mesh, n, perm, monkeypatch):
 
 KERNEL_SWITCHES = ["FEA_SLOT_NO_FIXED", "FEA_CN_NO_RECORDS", "FEA_D1_NO_DIRECT", "FEA_D1_NO_VEC",
                    "FEA_GATHER_NO_SLOT", "FEA_GATHER_NO_CN", "FEA_D1_NO_LANE", "FEA_D1_REC8",
-                   "FEA_D1_NO_LANE,FEA_D1_NO_DIRECT"]
+                   "FEA_D1_NO_LANE,FEA_D1_NO_DIRECT", "FEA_GATHER_GLOBAL"]
 
 
 @pytest.mark.parametrize("switch", KERNEL_SWITCHES)
