@@ -702,6 +702,37 @@ __global__ void k_node_of(const int64_t* __restrict__ adj_ptr, int64_t n_own, in
         for (int64_t k = adj_ptr[v]; k < adj_ptr[v + 1]; ++k) node_of[k] = static_cast<int32_t>(v);
 }
 
+// colour of every K row from the colour of every kept element (rows of other elements: 0)
+__global__ void k_colour_of_krow(const int32_t* __restrict__ elem_krow, const int32_t* __restrict__ col, int64_t E,
+                                 int32_t* __restrict__ colour_of_krow) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+        colour_of_krow[elem_krow[e]] = col[e];
+}
+
+// find_colour_conflict (colouring.cpp:91-119) as a yes / no question: does any owned node have two
+// different incident elements of one colour? (The offending pair is then named by the host scan,
+// in the reference's order; a valid colouring - the usual case - never reaches it.)
+__global__ void k_colour_conflict(const int64_t* __restrict__ adj_ptr, const int32_t* __restrict__ adj, int64_t n_own,
+                                  int npe, const int32_t* __restrict__ colour_of_krow, unsigned* __restrict__ flag) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n_own; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b0 = adj_ptr[v];
+        const int n = static_cast<int>(adj_ptr[v + 1] - b0);
+        bool bad = false;
+        for (int i = 1; i < n && !bad; ++i) {
+            const int32_t ki = adj[b0 + i] / npe;
+            const int32_t ci = colour_of_krow[ki];
+            for (int j = 0; j < i; ++j) {
+                const int32_t kj = adj[b0 + j] / npe;
+                if (kj != ki && colour_of_krow[kj] == ci) {
+                    bad = true;
+                    break;
+                }
+            }
+        }
+        if (bad) atomicOr(flag, 1u);
+    }
+}
+
 __global__ void k_colour_keys(const int32_t* __restrict__ adj, int64_t n_adj, int npe,
                               const int32_t* __restrict__ colour_of_krow, uint32_t* __restrict__ keys,
                               int32_t* __restrict__ vals) {
@@ -1517,26 +1548,14 @@ std::vector<int32_t> host_conn(const fea_plan* p, cudaStream_t s) {
 }
 
 // Per-node incidences in ascending (colour, element id) plus their position rows.
-void build_colour_incidences(fea_plan* p, const std::vector<int32_t>& colour_of_elem, cudaStream_t s) {
+void build_colour_incidences(fea_plan* p, const DevBuf& d_ck, int nc, cudaStream_t s) {
     const int64_t n = p->n_adj;
     const int row_bytes = p->pstride * p->pos_bytes;
     p->adjC.alloc(n * 4 + 64);
     p->posAC.alloc(n * row_bytes + 64);
     FEA_CK(cudaMemsetAsync(p->posAC.p, 0, p->posAC.bytes, s));
     if (n == 0) return;
-    // colour of every K row (kept elements; others never appear in the incidences)
-    std::vector<int32_t> kr(static_cast<size_t>(p->E));
-    if (p->E > 0)
-        FEA_CK(cudaMemcpy(kr.data(), p->elem_krow.p, kr.size() * 4, cudaMemcpyDeviceToHost));
-    std::vector<int32_t> ck(static_cast<size_t>(p->krows()), 0);
-    int nc = 1;
-    for (int64_t le = 0; le < p->E; ++le) {
-        ck[kr[le]] = colour_of_elem[le];
-        nc = std::max(nc, colour_of_elem[le] + 1);
-    }
-    DevBuf d_ck, node_of, k1, v1, k2, v2;
-    d_ck.alloc(ck.size() * 4);
-    FEA_CK(cudaMemcpyAsync(d_ck.p, ck.data(), ck.size() * 4, cudaMemcpyHostToDevice, s));
+    DevBuf node_of, k1, v1, k2, v2;
     node_of.alloc(n * 4);
     k1.alloc(n * 4); v1.alloc(n * 4); k2.alloc(n * 4); v2.alloc(n * 4);
     k_node_of<<<grid_for(p->n_own, 256), 256, 0, s>>>(p->adj_ptr.as<int64_t>(), p->n_own, node_of.as<int32_t>());
@@ -1938,9 +1957,28 @@ fea_status fea_plan_set_colouring(fea_plan* p, const int32_t* colour_of) {
             FEA_REQUIRE(c >= 0, FEA_ERR_INVALID, "negative colour");
             nc = std::max(nc, c + 1);
         }
-        // find_colour_conflict (colouring.cpp:91-119): same-colour elements may
-        // not share a DOF; with node-contiguous DOFs that is sharing a node.
-        const std::vector<int32_t> conn = host_conn(p, st.s);
+        // colour of every K row on the device, and the conflict question answered there (a node
+        // with two different incident elements of one colour); only an invalid colouring takes
+        // the host scan below, which names the pair the reference's scan would name
+        DevBuf d_col, d_ck, d_flag;
+        d_col.alloc(std::max<size_t>(col.size(), 1) * 4);
+        d_ck.alloc(std::max<int64_t>(p->krows(), 1) * 4);
+        d_flag.alloc(4);
+        FEA_CK(cudaMemsetAsync(d_ck.p, 0, d_ck.bytes, st.s));
+        FEA_CK(cudaMemsetAsync(d_flag.p, 0, 4, st.s));
+        unsigned conflict = 0;
+        if (p->E > 0) {
+            FEA_CK(cudaMemcpyAsync(d_col.p, col.data(), col.size() * 4, cudaMemcpyHostToDevice, st.s));
+            k_colour_of_krow<<<grid_for(p->E, 256), 256, 0, st.s>>>(p->elem_krow.as<int32_t>(), d_col.as<int32_t>(), p->E,
+                                                                   d_ck.as<int32_t>());
+            if (p->n_own > 0)
+                k_colour_conflict<<<grid_for(p->n_own, 128), 128, 0, st.s>>>(p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(),
+                                                                            p->n_own, p->npe, d_ck.as<int32_t>(),
+                                                                            d_flag.as<unsigned>());
+            FEA_CK(cudaGetLastError());
+            FEA_CK(cudaMemcpyAsync(&conflict, d_flag.p, 4, cudaMemcpyDeviceToHost, st.s));
+            FEA_CK(cudaStreamSynchronize(st.s));
+        }
         const int npe = p->npe;
         std::vector<int64_t> off(static_cast<size_t>(nc) + 1, 0);
         for (const int32_t c : col) ++off[c + 1];
@@ -1950,37 +1988,43 @@ fea_status fea_plan_set_colouring(fea_plan* p, const int32_t* colour_of) {
             std::vector<int64_t> f(off.begin(), off.end() - 1);
             for (int64_t e = 0; e < p->E; ++e) by_colour[f[col[e]]++] = static_cast<int32_t>(e);
         }
-        int64_t n_nodes = 0;
-        for (const int32_t v : conn) n_nodes = std::max<int64_t>(n_nodes, v + 1);
-        std::vector<int64_t> owner(static_cast<size_t>(n_nodes), -1);
-        for (int c = 0; c < nc; ++c) {
-            for (int64_t i = off[c]; i < off[c + 1]; ++i) {
-                const int32_t e = by_colour[i];
-                for (int a = 0; a < npe; ++a) {
-                    const int32_t v = conn[static_cast<int64_t>(e) * npe + a];
-                    // only owned rows are assembled: sharing a node outside them is no conflict
-                    if (v < p->node_begin || v >= p->node_end) continue;
-                    if (owner[v] >= 0 && owner[v] != e)
-                        throw Error(FEA_ERR_INVALID_COLOURING,
-                                    "invalid colouring: elements " + std::to_string(owner[v]) +
-                                        " and " + std::to_string(e) + " share dof " +
-                                        std::to_string(static_cast<int64_t>(v) * p->d) +
-                                        " within one colour");
-                    owner[v] = e;
+        if (conflict) {
+            // find_colour_conflict (colouring.cpp:91-119): same-colour elements may
+            // not share a DOF; with node-contiguous DOFs that is sharing a node.
+            const std::vector<int32_t> conn = host_conn(p, st.s);
+            int64_t n_nodes = 0;
+            for (const int32_t v : conn) n_nodes = std::max<int64_t>(n_nodes, v + 1);
+            std::vector<int64_t> owner(static_cast<size_t>(n_nodes), -1);
+            for (int c = 0; c < nc; ++c) {
+                for (int64_t i = off[c]; i < off[c + 1]; ++i) {
+                    const int32_t e = by_colour[i];
+                    for (int a = 0; a < npe; ++a) {
+                        const int32_t v = conn[static_cast<int64_t>(e) * npe + a];
+                        // only owned rows are assembled: sharing a node outside them is no conflict
+                        if (v < p->node_begin || v >= p->node_end) continue;
+                        if (owner[v] >= 0 && owner[v] != e)
+                            throw Error(FEA_ERR_INVALID_COLOURING,
+                                        "invalid colouring: elements " + std::to_string(owner[v]) +
+                                            " and " + std::to_string(e) + " share dof " +
+                                            std::to_string(static_cast<int64_t>(v) * p->d) +
+                                            " within one colour");
+                        owner[v] = e;
+                    }
                 }
+                for (int64_t i = off[c]; i < off[c + 1]; ++i)
+                    for (int a = 0; a < npe; ++a) {
+                        const int32_t v = conn[static_cast<int64_t>(by_colour[i]) * npe + a];
+                        if (v >= p->node_begin && v < p->node_end) owner[v] = -1;
+                    }
             }
-            for (int64_t i = off[c]; i < off[c + 1]; ++i)
-                for (int a = 0; a < npe; ++a) {
-                    const int32_t v = conn[static_cast<int64_t>(by_colour[i]) * npe + a];
-                    if (v >= p->node_begin && v < p->node_end) owner[v] = -1;
-                }
+            throw Error(FEA_ERR_INVALID_COLOURING, "invalid colouring: two elements of one colour share a dof");
         }
         p->colour_elems.alloc(by_colour.size() * 4);
         if (!by_colour.empty())
             FEA_CK(cudaMemcpy(p->colour_elems.p, by_colour.data(), by_colour.size() * 4,
                               cudaMemcpyHostToDevice));
         p->colour_off = off;
-        build_colour_incidences(p, col, st.s);
+        build_colour_incidences(p, d_ck, std::max(nc, 1), st.s);
         p->has_colouring = true;
     });
 }
