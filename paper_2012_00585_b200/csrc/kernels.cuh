@@ -2689,6 +2689,7 @@ __global__ void __launch_bounds__(256)
             auto add = [&](int b, int t) {
                 const int ki = t / d, kj = t - ki * d;
                 const double x = gen.on ? kgen_entry(he, a * d + ki, b * d + kj) : src[ki * m + b * d + kj];
+                FEA_DCHECK(static_cast<int64_t>(pos[b]) * d + kj < rowlen);
                 double* dst = blk + ki * rowlen + static_cast<int64_t>(pos[b]) * d + kj;
                 *dst += x;
             };

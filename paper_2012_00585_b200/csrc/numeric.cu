@@ -309,8 +309,9 @@ __global__ void __launch_bounds__(kPtWarps * 32)
 #pragma unroll
                 for (int b = 0; b < NPE; ++b) {
                     const int pos = static_cast<int>(((b < 4 ? pz.x : pz.y) >> (8 * (b & 3))) & 0xffu);
-                    out[b] = r[h] >= 0 ? static_cast<uint16_t>(patch_find(keys, n_pairs, (r[h] << 8) | pos))
-                                       : static_cast<uint16_t>(max_pairs);
+                    const int idx = r[h] >= 0 ? patch_find(keys, n_pairs, (r[h] << 8) | pos) : max_pairs;
+                    FEA_DCHECK(r[h] < 0 || (idx < n_pairs && keys[idx] == ((r[h] << 8) | pos)));
+                    out[b] = static_cast<uint16_t>(idx);
                 }
             }
         }
