@@ -581,138 +581,139 @@ void build_strips(fea_plan* p, cudaStream_t s) {
         int max_rows = 0, max_pairs = 0, max_ent = 0;
     };
     auto work = [&](int64_t q_begin, int64_t q_end, Part& part) {
-    std::vector<Shape>& shapes = part.shapes;
-    std::unordered_map<uint64_t, std::vector<int32_t>> by_hash;
-    std::vector<int64_t>& rows_all = part.rows_all;
-    std::vector<uint8_t>& ppos_all = part.ppos_all;
-    std::vector<uint16_t>&end_all = part.end_all, &ent_all = part.ent_all;
-    std::vector<uint8_t>& prow_all = part.prow_all;
-    int &max_rows = part.max_rows, &max_pairs = part.max_pairs, &max_ent = part.max_ent;
-    std::vector<int32_t> nstamp(nn, -1), nloc(nn, 0);
-    std::vector<int32_t> pstamp(static_cast<size_t>(P * NPE) * 256, -1);
-    std::vector<uint16_t> pidx(static_cast<size_t>(P * NPE) * 256, 0);
-    std::vector<uint8_t> kpos(static_cast<size_t>(P * NPE) * 256, 0);
-    std::vector<int32_t> keys, sorted, cnt, cnt2, ord;
-    std::vector<uint16_t> epair(P * NN), remap, newidx, t_end, t_ent;
-    std::vector<uint8_t> t_prow;
-    for (int64_t q = q_begin; q < q_end; ++q) {
-        const int n_el = static_cast<int>(std::min<int64_t>(P, E - q * P));
-        keys.clear();
-        int n_loc = 0;
-        bool contig = true;
-        const int64_t rows_off = static_cast<int64_t>(rows_all.size());
-        for (int k = 0; k < n_el; ++k) {  // local node numbers by first appearance
-            const int32_t le = order[q * P + k];
-            hkrow[q * P + k] = krow[le];
-            contig = contig && krow[le] == krow[order[q * P]] + k;
-            for (int a = 0; a < NPE; ++a) {
-                const int32_t v = conn[static_cast<size_t>(krow[le]) * NPE + a];
-                if (nstamp[v] != q) {
-                    nstamp[v] = static_cast<int32_t>(q);
-                    nloc[v] = n_loc++;
-                    const int64_t vo = static_cast<int64_t>(v) - p->node_begin;
-                    rows_all.push_back(vo >= 0 && vo < p->n_own ? nptr[vo] : -1);
+        std::vector<Shape>& shapes = part.shapes;
+        std::unordered_map<uint64_t, std::vector<int32_t>> by_hash;
+        std::vector<int64_t>& rows_all = part.rows_all;
+        std::vector<uint8_t>& ppos_all = part.ppos_all;
+        std::vector<uint16_t>& end_all = part.end_all;
+        std::vector<uint16_t>& ent_all = part.ent_all;
+        std::vector<uint8_t>& prow_all = part.prow_all;
+        int &max_rows = part.max_rows, &max_pairs = part.max_pairs, &max_ent = part.max_ent;
+        std::vector<int32_t> nstamp(nn, -1), nloc(nn, 0);
+        std::vector<int32_t> pstamp(static_cast<size_t>(P * NPE) * 256, -1);
+        std::vector<uint16_t> pidx(static_cast<size_t>(P * NPE) * 256, 0);
+        std::vector<uint8_t> kpos(static_cast<size_t>(P * NPE) * 256, 0);
+        std::vector<int32_t> keys, sorted, cnt, cnt2, ord;
+        std::vector<uint16_t> epair(P * NN), remap, newidx, t_end, t_ent;
+        std::vector<uint8_t> t_prow;
+        for (int64_t q = q_begin; q < q_end; ++q) {
+            const int n_el = static_cast<int>(std::min<int64_t>(P, E - q * P));
+            keys.clear();
+            int n_loc = 0;
+            bool contig = true;
+            const int64_t rows_off = static_cast<int64_t>(rows_all.size());
+            for (int k = 0; k < n_el; ++k) {  // local node numbers by first appearance
+                const int32_t le = order[q * P + k];
+                hkrow[q * P + k] = krow[le];
+                contig = contig && krow[le] == krow[order[q * P]] + k;
+                for (int a = 0; a < NPE; ++a) {
+                    const int32_t v = conn[static_cast<size_t>(krow[le]) * NPE + a];
+                    if (nstamp[v] != q) {
+                        nstamp[v] = static_cast<int32_t>(q);
+                        nloc[v] = n_loc++;
+                        const int64_t vo = static_cast<int64_t>(v) - p->node_begin;
+                        rows_all.push_back(vo >= 0 && vo < p->n_own ? nptr[vo] : -1);
+                    }
                 }
             }
-        }
-        for (int k = 0; k < n_el; ++k) {
-            const int32_t le = order[q * P + k];
-            const int32_t* cv = conn.data() + static_cast<size_t>(krow[le]) * NPE;
-            for (int a = 0; a < NPE; ++a) {
-                const int r = nloc[cv[a]];
-                const bool owned = rows_all[rows_off + r] >= 0;
-                for (int b = 0; b < NPE; ++b) {
-                    if (!owned) {  // row not owned: its entries are dropped
-                        epair[k * NN + a * NPE + b] = 0xffffu;
-                        continue;
+            for (int k = 0; k < n_el; ++k) {
+                const int32_t le = order[q * P + k];
+                const int32_t* cv = conn.data() + static_cast<size_t>(krow[le]) * NPE;
+                for (int a = 0; a < NPE; ++a) {
+                    const int r = nloc[cv[a]];
+                    const bool owned = rows_all[rows_off + r] >= 0;
+                    for (int b = 0; b < NPE; ++b) {
+                        if (!owned) {  // row not owned: its entries are dropped
+                            epair[k * NN + a * NPE + b] = 0xffffu;
+                            continue;
+                        }
+                        const int key = r * 256 + nloc[cv[b]];
+                        if (pstamp[key] != q) {
+                            pstamp[key] = static_cast<int32_t>(q);
+                            pidx[key] = static_cast<uint16_t>(keys.size());
+                            kpos[key] = posE[static_cast<size_t>(le) * NN + a * NPE + b];
+                            keys.push_back(key);
+                        }
+                        epair[k * NN + a * NPE + b] = pidx[key];
                     }
-                    const int key = r * 256 + nloc[cv[b]];
-                    if (pstamp[key] != q) {
-                        pstamp[key] = static_cast<int32_t>(q);
-                        pidx[key] = static_cast<uint16_t>(keys.size());
-                        kpos[key] = posE[static_cast<size_t>(le) * NN + a * NPE + b];
-                        keys.push_back(key);
-                    }
-                    epair[k * NN + a * NPE + b] = pidx[key];
                 }
             }
-        }
-        // pairs sorted by (local row, local column); entry lists by counting sort (ascending offset)
-        sorted = keys;
-        std::sort(sorted.begin(), sorted.end());
-        remap.resize(keys.size());
-        for (size_t i = 0; i < sorted.size(); ++i) pidx[sorted[i]] = static_cast<uint16_t>(i);
-        for (size_t i = 0; i < keys.size(); ++i) remap[i] = pidx[keys[i]];
-        const int n_pairs = static_cast<int>(sorted.size());
-        cnt.assign(n_pairs + 1, 0);
-        int n_ent = 0;
-        for (int x = 0; x < n_el * NN; ++x)
-            if (epair[x] != 0xffffu) {
-                epair[x] = remap[epair[x]];
-                ++cnt[epair[x] + 1];
-                ++n_ent;
+            // pairs sorted by (local row, local column); entry lists by counting sort (ascending offset)
+            sorted = keys;
+            std::sort(sorted.begin(), sorted.end());
+            remap.resize(keys.size());
+            for (size_t i = 0; i < sorted.size(); ++i) pidx[sorted[i]] = static_cast<uint16_t>(i);
+            for (size_t i = 0; i < keys.size(); ++i) remap[i] = pidx[keys[i]];
+            const int n_pairs = static_cast<int>(sorted.size());
+            cnt.assign(n_pairs + 1, 0);
+            int n_ent = 0;
+            for (int x = 0; x < n_el * NN; ++x)
+                if (epair[x] != 0xffffu) {
+                    epair[x] = remap[epair[x]];
+                    ++cnt[epair[x] + 1];
+                    ++n_ent;
+                }
+            // thread t of the CTA sums pair t's list, and a warp runs as long as its longest list:
+            // the long lists (a node's diagonal collects an entry from each of its elements in the
+            // strip, up to 24 on a Kuhn mesh; an edge 1-6) go first, longest first, so they share
+            // warps; the short ones keep the (row, column) order, whose neighbours share sectors
+            ord.resize(n_pairs);
+            for (int i = 0; i < n_pairs; ++i) ord[i] = i;
+            std::stable_sort(ord.begin(), ord.end(), [&](int i, int j) {
+                const int li = cnt[i + 1], lj = cnt[j + 1];
+                if (long_len <= 0) return li > lj;  // FEA_STRIP_LONG=0: all by length
+                if ((li > long_len) != (lj > long_len)) return li > long_len;
+                return li > long_len ? li > lj : false;
+            });
+            newidx.resize(n_pairs);
+            for (int k = 0; k < n_pairs; ++k) newidx[ord[k]] = static_cast<uint16_t>(k);
+            cnt2.assign(n_pairs + 1, 0);
+            for (int k = 0; k < n_pairs; ++k) cnt2[k + 1] = cnt2[k] + cnt[ord[k] + 1];
+            t_end.resize(n_pairs);
+            t_prow.resize(n_pairs);
+            t_ent.resize(n_ent);
+            const int64_t pairs_off = static_cast<int64_t>(ppos_all.size());
+            for (int k = 0; k < n_pairs; ++k) {
+                t_end[k] = static_cast<uint16_t>(cnt2[k + 1]);
+                t_prow[k] = static_cast<uint8_t>(sorted[ord[k]] >> 8);
+                ppos_all.push_back(kpos[sorted[ord[k]]]);
             }
-        // thread t of the CTA sums pair t's list, and a warp runs as long as its longest list:
-        // the long lists (a node's diagonal collects an entry from each of its elements in the
-        // strip, up to 24 on a Kuhn mesh; an edge 1-6) go first, longest first, so they share
-        // warps; the short ones keep the (row, column) order, whose neighbours share sectors
-        ord.resize(n_pairs);
-        for (int i = 0; i < n_pairs; ++i) ord[i] = i;
-        std::stable_sort(ord.begin(), ord.end(), [&](int i, int j) {
-            const int li = cnt[i + 1], lj = cnt[j + 1];
-            if (long_len <= 0) return li > lj;  // FEA_STRIP_LONG=0: all by length
-            if ((li > long_len) != (lj > long_len)) return li > long_len;
-            return li > long_len ? li > lj : false;
-        });
-        newidx.resize(n_pairs);
-        for (int k = 0; k < n_pairs; ++k) newidx[ord[k]] = static_cast<uint16_t>(k);
-        cnt2.assign(n_pairs + 1, 0);
-        for (int k = 0; k < n_pairs; ++k) cnt2[k + 1] = cnt2[k] + cnt[ord[k] + 1];
-        t_end.resize(n_pairs);
-        t_prow.resize(n_pairs);
-        t_ent.resize(n_ent);
-        const int64_t pairs_off = static_cast<int64_t>(ppos_all.size());
-        for (int k = 0; k < n_pairs; ++k) {
-            t_end[k] = static_cast<uint16_t>(cnt2[k + 1]);
-            t_prow[k] = static_cast<uint8_t>(sorted[ord[k]] >> 8);
-            ppos_all.push_back(kpos[sorted[ord[k]]]);
-        }
-        for (int x = 0; x < n_el * NN; ++x)
-            if (epair[x] != 0xffffu) t_ent[cnt2[newidx[epair[x]]]++] = static_cast<uint16_t>(x);
-        // shape de-duplication by content
-        uint64_t h = 1469598103934665603ull ^ static_cast<uint64_t>(n_pairs) * 1099511628211ull;
-        auto mixin = [&](const void* d, size_t n) {
-            const unsigned char* c = static_cast<const unsigned char*>(d);
-            for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ull;
-        };
-        mixin(t_end.data(), t_end.size() * 2);
-        mixin(t_prow.data(), t_prow.size());
-        mixin(t_ent.data(), t_ent.size() * 2);
-        int32_t shape = -1;
-        for (int32_t c : by_hash[h]) {
-            const Shape& sh = shapes[c];
-            if (sh.n_pairs == n_pairs && sh.n_ent == n_ent &&
-                std::memcmp(end_all.data() + sh.pairs_off, t_end.data(), n_pairs * 2) == 0 &&
-                std::memcmp(prow_all.data() + sh.pairs_off, t_prow.data(), n_pairs) == 0 &&
-                std::memcmp(ent_all.data() + sh.ent_off, t_ent.data(), n_ent * 2) == 0) {
-                shape = c;
-                break;
+            for (int x = 0; x < n_el * NN; ++x)
+                if (epair[x] != 0xffffu) t_ent[cnt2[newidx[epair[x]]]++] = static_cast<uint16_t>(x);
+            // shape de-duplication by content
+            uint64_t h = 1469598103934665603ull ^ static_cast<uint64_t>(n_pairs) * 1099511628211ull;
+            auto mixin = [&](const void* d, size_t n) {
+                const unsigned char* c = static_cast<const unsigned char*>(d);
+                for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ull;
+            };
+            mixin(t_end.data(), t_end.size() * 2);
+            mixin(t_prow.data(), t_prow.size());
+            mixin(t_ent.data(), t_ent.size() * 2);
+            int32_t shape = -1;
+            for (int32_t c : by_hash[h]) {
+                const Shape& sh = shapes[c];
+                if (sh.n_pairs == n_pairs && sh.n_ent == n_ent &&
+                    std::memcmp(end_all.data() + sh.pairs_off, t_end.data(), n_pairs * 2) == 0 &&
+                    std::memcmp(prow_all.data() + sh.pairs_off, t_prow.data(), n_pairs) == 0 &&
+                    std::memcmp(ent_all.data() + sh.ent_off, t_ent.data(), n_ent * 2) == 0) {
+                    shape = c;
+                    break;
+                }
             }
+            if (shape < 0) {
+                shape = static_cast<int32_t>(shapes.size());
+                shapes.push_back({static_cast<int64_t>(end_all.size()), static_cast<int64_t>(ent_all.size()), n_pairs, n_ent});
+                end_all.insert(end_all.end(), t_end.begin(), t_end.end());
+                prow_all.insert(prow_all.end(), t_prow.begin(), t_prow.end());
+                ent_all.insert(ent_all.end(), t_ent.begin(), t_ent.end());
+                by_hash[h].push_back(shape);
+            }
+            st[q] = {rows_off, pairs_off, n_loc, n_pairs, n_ent, n_el, shape};
+            hk0[q] = make_int4(contig ? krow[order[q * P]] : -1, n_el, shape, 0);
+            max_rows = std::max(max_rows, n_loc);
+            max_pairs = std::max(max_pairs, n_pairs);
+            max_ent = std::max(max_ent, n_ent);
         }
-        if (shape < 0) {
-            shape = static_cast<int32_t>(shapes.size());
-            shapes.push_back({static_cast<int64_t>(end_all.size()), static_cast<int64_t>(ent_all.size()), n_pairs, n_ent});
-            end_all.insert(end_all.end(), t_end.begin(), t_end.end());
-            prow_all.insert(prow_all.end(), t_prow.begin(), t_prow.end());
-            ent_all.insert(ent_all.end(), t_ent.begin(), t_ent.end());
-            by_hash[h].push_back(shape);
-        }
-        st[q] = {rows_off, pairs_off, n_loc, n_pairs, n_ent, n_el, shape};
-        hk0[q] = make_int4(contig ? krow[order[q * P]] : -1, n_el, shape, 0);
-        max_rows = std::max(max_rows, n_loc);
-        max_pairs = std::max(max_pairs, n_pairs);
-        max_ent = std::max(max_ent, n_ent);
-    }
     };
     const int n_thr = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>({int64_t{16}, static_cast<int64_t>(std::thread::hardware_concurrency()), n_strip / 1024})));
