@@ -336,14 +336,202 @@ __global__ void k_max2_i64(const int64_t* __restrict__ a, const int64_t* __restr
     }
 }
 
+// --- patches as node stars, found on the device ----------------------------------------------------
+// A 2 x 2 x 2 block of hex8 elements is the star of its centre node. On a plan that owns every
+// row the patches can therefore be found without the host's sequential sweep: candidates are the
+// nodes with exactly P incident elements, the chosen centres are the lexicographically first
+// maximal independent set of candidates in the node graph (two nodes that share an element are
+// neighbours - the pattern's rows - so chosen stars are disjoint), found by rounds: an undecided
+// candidate is chosen once every lower-numbered neighbouring candidate is out, and is out once one
+// of them is chosen. On a structured mesh in lexicographic numbering that is the host sweep's
+// tiling (centres at odd coordinates) in ~n rounds. The route is taken only if the stars cover
+// every element (even element counts per direction); anything else keeps the host sweep.
+__global__ void k_star_init(const int64_t* __restrict__ adj_ptr, int64_t n, int P, uint8_t* __restrict__ state) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        state[v] = adj_ptr[v + 1] - adj_ptr[v] == P ? 0 : 2;  // 0 undecided, 1 chosen, 2 out
+}
+__global__ void k_star_round(const int64_t* __restrict__ nptr, const int32_t* __restrict__ ncol, int64_t n,
+                             volatile uint8_t* state, unsigned long long* __restrict__ undecided) {
+    unsigned long long mine = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        if (state[v] != 0) continue;
+        bool wait = false, kill = false;
+        for (int64_t j = nptr[v]; j < nptr[v + 1]; ++j) {
+            const int32_t u = ncol[j];
+            if (u >= v) break;  // ascending: only lower-numbered neighbours decide
+            const uint8_t su = state[u];  // a stale "undecided" only delays the decision by a round
+            kill = kill || su == 1;
+            wait = wait || su == 0;
+        }
+        if (kill) state[v] = 2;
+        else if (!wait) state[v] = 1;
+        else ++mine;
+    }
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(undecided, mine);
+}
+__global__ void k_star_flags(const uint8_t* __restrict__ state, int64_t n, int64_t* __restrict__ flag) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= n; v += (int64_t)gridDim.x * blockDim.x)
+        flag[v] = v < n && state[v] == 1;
+}
+// members of every chosen star (its incident elements in adjacency order) and the patch of each
+__global__ void k_star_members(const uint8_t* __restrict__ state, const int64_t* __restrict__ idx, int64_t n,
+                               const int64_t* __restrict__ adj_ptr, const int32_t* __restrict__ adj, int npe, int P,
+                               int32_t* __restrict__ members, int32_t* __restrict__ patch_of) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        if (state[v] != 1) continue;
+        const int64_t q = idx[v], b0 = adj_ptr[v];
+        // slot of an element = where the centre sits in it: for the usual hex8 local numbering the
+        // order below walks the block's elements lexicographically, whatever their ids are (the
+        // host sweep's order; by ascending id cfg2's permuted elements measured 2.5 % slower)
+        const int rank[8] = {7, 6, 4, 5, 3, 2, 0, 1};
+        int32_t slot[8];
+        for (int k = 0; k < 8; ++k) slot[k] = -1;
+        for (int k = 0; k < P; ++k) {
+            const int32_t entry = adj[b0 + k];
+            const int a = entry % npe;
+            if (a < 8 && slot[rank[a]] < 0) slot[rank[a]] = entry / npe;  // the plan owns every row: K row = element
+        }
+        for (int k = 0; k < P; ++k) {  // two elements with the centre at the same local node: first free slot
+            const int32_t entry = adj[b0 + k];
+            const int a = entry % npe;
+            if (a < 8 && slot[rank[a]] == entry / npe) continue;
+            for (int f = 0; f < P; ++f)
+                if (slot[f] < 0) {
+                    slot[f] = entry / npe;
+                    break;
+                }
+        }
+        for (int k = 0; k < P; ++k) {
+            members[q * P + k] = slot[k];
+            patch_of[slot[k]] = static_cast<int32_t>(q);
+        }
+    }
+}
+// offsets nb - q of the patches nb > q that share a node with sampled patch q (0: none), 64 x 8 slots
+__global__ void k_patch_later(const int64_t* __restrict__ samples, const int32_t* __restrict__ members,
+                              const int32_t* __restrict__ conn_k, const int64_t* __restrict__ adj_ptr,
+                              const int32_t* __restrict__ adj, const int32_t* __restrict__ patch_of, int npe, int P,
+                              int64_t* __restrict__ out) {
+    const int64_t q = samples[blockIdx.x];
+    const int t = threadIdx.x, k = t / npe, a = t - k * npe;  // blockDim = P * npe
+    int64_t* o = out + (static_cast<int64_t>(blockIdx.x) * blockDim.x + t) * 8;
+    for (int j = 0; j < 8; ++j) o[j] = 0;
+    const int32_t le = members[q * P + k];
+    if (le < 0) return;
+    const int64_t v = conn_k[static_cast<int64_t>(le) * npe + a];
+    const int64_t b0 = adj_ptr[v];
+    const int n = static_cast<int>(min(adj_ptr[v + 1] - b0, static_cast<int64_t>(8)));
+    for (int j = 0; j < n; ++j) {
+        const int64_t nb = patch_of[adj[b0 + j] / npe];
+        o[j] = nb > q ? nb - q : 0;
+    }
+}
+__global__ void k_permute_members(const int32_t* __restrict__ seq, const int32_t* __restrict__ in, int64_t n, int P,
+                                  int32_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * P; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[static_cast<int64_t>(seq[i / P]) * P + i % P];
+}
+
 // Patches of k_atomic_patch (npe = 8, d <= 3, byte positions, no repeated nodes): greedy growth
 // from the atomic visit order — the first unassigned element, then repeatedly the unassigned
 // element sharing the most nodes with the patch (ties: earlier in the visit order) — up to
 // kPatchElems elements; on structured hex8 meshes this tiles 2 x 2 x 2 blocks. Per patch the
 // distinct (owned row node, column node) pairs, sorted by (row, position), and per element the
-// pair index of each (a, b). Once per plan, on the first atomic assembly: the greedy growth (a
-// sequential sweep) and the lattice order run on the host, the tables are built on the device
-// (k_patch_tables; 12 s of a 16 s first call on config 5 when they were built on one host thread).
+// pair index of each (a, b). Once per plan, on the first atomic assembly. Where the node stars
+// tile the mesh the patches are found on the device (star_patches); otherwise the greedy growth
+// (a sequential sweep) and the lattice order run on the host. The tables are built on the device
+// either way (k_patch_tables; 12 s of a 16 s first call on config 5 when one host thread built them).
+// Device route of build_patches (see k_star_init). false: the stars do not tile the mesh.
+bool star_patches(fea_plan* p, DevBuf& d_mem, int64_t* n_patch_out, cudaStream_t s) {
+    constexpr int P = kPatchElems;
+    const int64_t n = p->n_own, E = p->E;
+    if (p->partitioned || n == 0 || p->n_adj != E * p->npe || std::getenv("FEA_PATCH_HOST_SWEEP")) return false;
+    DevBuf state, cnt, flag, idx, patch_of, bad;
+    state.alloc(n);
+    cnt.alloc(8);
+    k_star_init<<<grid_for(n, 256), 256, 0, s>>>(p->adj_ptr.as<int64_t>(), n, P, state.as<uint8_t>());
+    FEA_CK(cudaGetLastError());
+    for (int round = 0;; round += 8) {  // 8 rounds per look at the counter
+        FEA_REQUIRE(round < (1 << 22), FEA_ERR_INVALID, "internal: star selection does not converge");
+        unsigned long long left = 0;
+        for (int r = 0; r < 8; ++r) {
+            FEA_CK(cudaMemsetAsync(cnt.p, 0, 8, s));
+            k_star_round<<<grid_for(n, 256), 256, 0, s>>>(p->nptr.as<int64_t>(), p->ncol.as<int32_t>(), n,
+                                                         state.as<uint8_t>(), cnt.as<unsigned long long>());
+        }
+        FEA_CK(cudaGetLastError());
+        FEA_CK(cudaMemcpyAsync(&left, cnt.p, 8, cudaMemcpyDeviceToHost, s));
+        FEA_CK(cudaStreamSynchronize(s));
+        if (left == 0) break;
+    }
+    flag.alloc((n + 1) * 8);
+    idx.alloc((n + 1) * 8);
+    k_star_flags<<<grid_for(n + 1, 256), 256, 0, s>>>(state.as<uint8_t>(), n, flag.as<int64_t>());
+    exclusive_sum(flag.as<int64_t>(), idx.as<int64_t>(), n + 1, s);
+    int64_t n_patch = 0;
+    FEA_CK(cudaMemcpyAsync(&n_patch, idx.as<int64_t>() + n, 8, cudaMemcpyDeviceToHost, s));
+    FEA_CK(cudaStreamSynchronize(s));
+    if (n_patch * P != E) return false;  // disjoint stars of P elements each: they cover the mesh iff the counts agree
+    d_mem.alloc(static_cast<size_t>(n_patch) * P * 4);
+    patch_of.alloc(static_cast<size_t>(E) * 4);
+    k_star_members<<<grid_for(n, 256), 256, 0, s>>>(state.as<uint8_t>(), idx.as<int64_t>(), n, p->adj_ptr.as<int64_t>(),
+                                                   p->adj.as<int32_t>(), p->npe, P, d_mem.as<int32_t>(),
+                                                   patch_of.as<int32_t>());
+    FEA_CK(cudaGetLastError());
+    // lattice order of the patch sequence (as in the host route): later neighbours of the sampled
+    // patches from a small kernel, the tile permutation applied on the device
+    if (!std::getenv("FEA_PATCH_NO_TILES")) {
+        std::vector<int64_t> samples;
+        for (int smp = 0; smp < 64; ++smp) samples.push_back((n_patch / 2 + smp * (std::max<int64_t>(n_patch / 67, 1) | 1)) % n_patch);
+        for (int smp = 0; smp < 257; ++smp) samples.push_back((n_patch - 1) * smp / 256);
+        const int threads = P * p->npe;
+        DevBuf d_s, d_o;
+        d_s.alloc(samples.size() * 8);
+        d_o.alloc(samples.size() * threads * 8 * 8);
+        FEA_CK(cudaMemcpyAsync(d_s.p, samples.data(), samples.size() * 8, cudaMemcpyHostToDevice, s));
+        k_patch_later<<<static_cast<unsigned>(samples.size()), threads, 0, s>>>(
+            d_s.as<int64_t>(), d_mem.as<int32_t>(), p->conn_k.as<int32_t>(), p->adj_ptr.as<int64_t>(), p->adj.as<int32_t>(),
+            patch_of.as<int32_t>(), p->npe, P, d_o.as<int64_t>());
+        FEA_CK(cudaGetLastError());
+        std::vector<int64_t> h_o(samples.size() * threads * 8);
+        FEA_CK(cudaMemcpyAsync(h_o.data(), d_o.p, h_o.size() * 8, cudaMemcpyDeviceToHost, s));
+        FEA_CK(cudaStreamSynchronize(s));
+        auto later = [&](int64_t q, std::vector<int64_t>& offs) {
+            offs.clear();
+            const size_t i = static_cast<size_t>(std::find(samples.begin(), samples.end(), q) - samples.begin());
+            if (i == samples.size()) return;
+            for (int t = 0; t < threads * 8; ++t)
+                if (h_o[i * threads * 8 + t] > 0) offs.push_back(h_o[i * threads * 8 + t]);
+            std::sort(offs.begin(), offs.end());
+            offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+        };
+        int64_t s1 = 0, s2 = 0;
+        const bool lattice = detect_lattice(n_patch, later, &s1, &s2);
+        const int64_t plane_k = s2 * P * static_cast<int64_t>(p->m) * p->m * 8;
+        if (std::getenv("FEA_PATCH_DEBUG"))
+            std::fprintf(stderr, "patch lattice (stars): n_patch %lld s1 %lld s2 %lld lattice %d plane_k %lld\n",
+                         (long long)n_patch, (long long)s1, (long long)s2, (int)lattice, (long long)plane_k);
+        const char* tile_env = std::getenv("FEA_PATCH_TILE");
+        if (lattice && (plane_k > (int64_t{64} << 20) || tile_env)) {
+            const std::vector<int32_t> seq = tiled_sequence(n_patch, s1, s2, tile_env ? std::max(1, std::atoi(tile_env)) : 16);
+            DevBuf d_seq, d_m2;
+            d_seq.alloc(seq.size() * 4);
+            d_m2.alloc(d_mem.bytes);
+            FEA_CK(cudaMemcpyAsync(d_seq.p, seq.data(), seq.size() * 4, cudaMemcpyHostToDevice, s));
+            k_permute_members<<<grid_for(n_patch * P, 256), 256, 0, s>>>(d_seq.as<int32_t>(), d_mem.as<int32_t>(), n_patch, P,
+                                                                        d_m2.as<int32_t>());
+            FEA_CK(cudaGetLastError());
+            FEA_CK(cudaStreamSynchronize(s));
+            d_mem = std::move(d_m2);
+        }
+    } else if (std::getenv("FEA_PATCH_DEBUG")) {
+        std::fprintf(stderr, "patch stars: n_patch %lld\n", (long long)n_patch);
+    }
+    *n_patch_out = n_patch;
+    return true;
+}
+
 void build_patches(fea_plan* p, cudaStream_t s) {
     if (p->npe != 8 || p->d > 3 || p->pos_bytes != 1 || p->dup_nodes || p->E == 0 || p->kn.atomic_no_patch ||
         p->kn.atomic_legacy || p->pk_n > 0)
@@ -359,6 +547,11 @@ void build_patches(fea_plan* p, cudaStream_t s) {
                      std::chrono::duration<double, std::milli>(now - t_last).count());
         t_last = now;
     };
+    DevBuf d_mem;
+    int64_t n_patch = 0;
+    const bool on_device = star_patches(p, d_mem, &n_patch, s);
+    if (on_device) mark("star patches (device)");
+    if (!on_device) {
     std::vector<int32_t> order(E), krow(E), conn(static_cast<size_t>(p->krows() * NPE));
     FEA_CK(cudaMemcpyAsync(order.data(), p->order.p, E * 4, cudaMemcpyDeviceToHost, s));
     FEA_CK(cudaMemcpyAsync(krow.data(), p->elem_krow.p, E * 4, cudaMemcpyDeviceToHost, s));
@@ -426,7 +619,7 @@ void build_patches(fea_plan* p, cudaStream_t s) {
         for (; n_m < P; ++n_m) members.push_back(-1);
         ++pid;
     }
-    const int64_t n_patch = pid;
+    n_patch = pid;
     mark("greedy growth");
     // Tiled visit order for lattice-like patch sequences (a structured mesh in lexicographic
     // order: patch q shares nodes with q + 1, q + s1 +- 1, q + s2 +- s1 +- 1). In sequence order
@@ -475,11 +668,13 @@ void build_patches(fea_plan* p, cudaStream_t s) {
         }
     }
     mark("lattice + tiles");
-    // per patch: rows, pairs, element pair indices - on the device (k_patch_tables): a count pass,
-    // two exclusive scans for the row and pair offsets, a fill pass
-    DevBuf d_mem, d_nr, d_np, d_ro, d_po, d_mx;
     d_mem.alloc(members.size() * 4);
     FEA_CK(cudaMemcpyAsync(d_mem.p, members.data(), members.size() * 4, cudaMemcpyHostToDevice, s));
+    FEA_CK(cudaStreamSynchronize(s));
+    }
+    // per patch: rows, pairs, element pair indices - on the device (k_patch_tables): a count pass,
+    // two exclusive scans for the row and pair offsets, a fill pass
+    DevBuf d_nr, d_np, d_ro, d_po, d_mx;
     d_nr.alloc((n_patch + 1) * 8);
     d_np.alloc((n_patch + 1) * 8);
     d_ro.alloc((n_patch + 1) * 8);

@@ -726,12 +726,14 @@ def test_lane_owned_slots_shapes(gpu, orc):
 
 
 @pytest.mark.parametrize("env", [{"FEA_PATCH_TICKETS": "1"}, {"FEA_PATCH_TICKETS": "1", "FEA_PATCH_TILE": "2"},
-                                 {"FEA_PATCH_STATIC": "1", "FEA_PATCH_TILE": "3"}, {"FEA_PATCH_NO_TILES": "1"}])
+                                 {"FEA_PATCH_STATIC": "1", "FEA_PATCH_TILE": "3"}, {"FEA_PATCH_NO_TILES": "1"},
+                                 {"FEA_PATCH_HOST_SWEEP": "1"}, {"FEA_PATCH_HOST_SWEEP": "1", "FEA_PATCH_TILE": "2"}])
 @pytest.mark.parametrize("n,perm", [(8, None), (7, None), (6, "elements")])
 def test_atomic_patch_schedules(gpu, orc, env, n, perm, monkeypatch):
     """k_atomic_patch under every patch schedule: tickets / grid stride, lattice tiles of several
     sizes (forced on a small lexicographic mesh, where the detection finds s1 = n/2, s2 = (n/2)^2)
-    or the sequence order. Any order is a valid atomic assembly: within the reference tolerance of
+    or the sequence order; patches found on the device as node stars (even n) or by the host sweep
+    (odd n, or forced). Any order is a valid atomic assembly: within the reference tolerance of
     the sequential result, and bitwise with ones (every sum is exact)."""
     import torch
     for k, v in env.items():
