@@ -752,6 +752,33 @@ def test_atomic_patch_schedules(gpu, orc, env, n, perm, monkeypatch):
         assert got1.tobytes() == want1.tobytes()
 
 
+@pytest.mark.parametrize("dims,perm_nodes", [((2, 2, 40), False), ((4, 2, 6), True), ((6, 4, 2), False), ((3, 4, 4), False)])
+def test_atomic_star_patches_boxes(gpu, orc, dims, perm_nodes, monkeypatch, capfd):
+    """Patches found on the device as node stars on non-cubic boxes: a thin bar (a long chain of
+    selection rounds), permuted node ids (another independent set, still a tiling or else the host
+    sweep), an odd direction (stars leave elements over: host sweep). Atomic within the reference
+    tolerance, bitwise with ones."""
+    import torch
+    monkeypatch.setenv("FEA_PATCH_DEBUG", "1")
+    conn, nn = M.hex8_box(*dims)
+    if perm_nodes:
+        conn = np.random.default_rng(3).permutation(nn)[conn]
+    ed = M.element_dofs(conn, 3)
+    P = orc.Pattern.build(conn, nn, 3)
+    Kh = orc.fill_k(6, conn.shape[0], ed.shape[1])
+    want = P.assemble_sequential(ed, Kh)
+    ones = np.ones_like(Kh)
+    with gpu.Plan(ed, nn * 3, dofs_per_node=3) as plan:
+        assert close(plan.assemble(torch.from_numpy(Kh).cuda(), strategy="atomic").cpu().numpy(), want)
+        got1 = plan.assemble(torch.from_numpy(ones).cuda(), strategy="atomic").cpu().numpy()
+        assert got1.tobytes() == P.assemble_sequential(ed, ones).tobytes()
+    err = capfd.readouterr().err
+    if not perm_nodes and all(x % 2 == 0 for x in dims):
+        assert "(stars)" in err, err  # lexicographic even boxes are tiled by the stars
+    if any(x % 2 for x in dims):
+        assert "(stars)" not in err, err
+
+
 @pytest.mark.parametrize("env", [{}, {"FEA_PATCH_TICKETS": "1"}, {"FEA_STRIP_LONG": "0"}, {"FEA_ATOMIC_NO_STRIP": "1"}])
 @pytest.mark.parametrize("mesh,n,perm", [("tet4", 5, "nodes"), ("tet4", 4, "elements"), ("quad4", 13, "elements"),
                                          ("quad4", 9, None)])
