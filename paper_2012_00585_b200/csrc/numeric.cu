@@ -427,6 +427,17 @@ __global__ void k_patch_later(const int64_t* __restrict__ samples, const int32_t
         o[j] = nb > q ? nb - q : 0;
     }
 }
+// tiled_sequence on the device: the key (tile, z, position in the tile) of item vals[i], one part
+// per stable radix pass (least significant part first)
+__global__ void k_tile_key(const int32_t* __restrict__ vals, int64_t n, int64_t s1, int64_t s2, int T, int part,
+                           uint32_t* __restrict__ keys) {
+    const int64_t tiles_x = (s1 + T - 1) / T;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = vals ? vals[i] : i;
+        const int64_t x = q % s1, y = (q % s2) / s1, z = q / s2;
+        keys[i] = static_cast<uint32_t>(part == 0 ? (y % T) * T + x % T : part == 1 ? z : (y / T) * tiles_x + x / T);
+    }
+}
 __global__ void k_permute_members(const int32_t* __restrict__ seq, const int32_t* __restrict__ in, int64_t n, int P,
                                   int32_t* __restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * P; i += (int64_t)gridDim.x * blockDim.x)
@@ -447,6 +458,16 @@ bool star_patches(fea_plan* p, DevBuf& d_mem, int64_t* n_patch_out, cudaStream_t
     constexpr int P = kPatchElems;
     const int64_t n = p->n_own, E = p->E;
     if (p->partitioned || n == 0 || p->n_adj != E * p->npe || std::getenv("FEA_PATCH_HOST_SWEEP")) return false;
+    const bool trace = std::getenv("FEA_PLAN_TRACE") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "star trace:  %-28s %9.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     DevBuf state, cnt, flag, idx, patch_of, bad;
     state.alloc(n);
     cnt.alloc(8);
@@ -465,6 +486,7 @@ bool star_patches(fea_plan* p, DevBuf& d_mem, int64_t* n_patch_out, cudaStream_t
         FEA_CK(cudaStreamSynchronize(s));
         if (left == 0) break;
     }
+    mark("selection rounds");
     flag.alloc((n + 1) * 8);
     idx.alloc((n + 1) * 8);
     k_star_flags<<<grid_for(n + 1, 256), 256, 0, s>>>(state.as<uint8_t>(), n, flag.as<int64_t>());
@@ -479,6 +501,7 @@ bool star_patches(fea_plan* p, DevBuf& d_mem, int64_t* n_patch_out, cudaStream_t
                                                    p->adj.as<int32_t>(), p->npe, P, d_mem.as<int32_t>(),
                                                    patch_of.as<int32_t>());
     FEA_CK(cudaGetLastError());
+    mark("members");
     // lattice order of the patch sequence (as in the host route): later neighbours of the sampled
     // patches from a small kernel, the tile permutation applied on the device
     if (!std::getenv("FEA_PATCH_NO_TILES")) {
@@ -508,17 +531,37 @@ bool star_patches(fea_plan* p, DevBuf& d_mem, int64_t* n_patch_out, cudaStream_t
         };
         int64_t s1 = 0, s2 = 0;
         const bool lattice = detect_lattice(n_patch, later, &s1, &s2);
+        mark("lattice detection");
         const int64_t plane_k = s2 * P * static_cast<int64_t>(p->m) * p->m * 8;
         if (std::getenv("FEA_PATCH_DEBUG"))
             std::fprintf(stderr, "patch lattice (stars): n_patch %lld s1 %lld s2 %lld lattice %d plane_k %lld\n",
                          (long long)n_patch, (long long)s1, (long long)s2, (int)lattice, (long long)plane_k);
         const char* tile_env = std::getenv("FEA_PATCH_TILE");
         if (lattice && (plane_k > (int64_t{64} << 20) || tile_env)) {
-            const std::vector<int32_t> seq = tiled_sequence(n_patch, s1, s2, tile_env ? std::max(1, std::atoi(tile_env)) : 16);
-            DevBuf d_seq, d_m2;
-            d_seq.alloc(seq.size() * 4);
+            // tiled_sequence(): three stable radix passes over the key parts instead of a host sort
+            const int T = tile_env ? std::max(1, std::atoi(tile_env)) : 16;
+            const int64_t tiles = ((s1 + T - 1) / T) * ((s2 / s1 + T - 1) / T), nz = (n_patch + s2 - 1) / s2;
+            DevBuf d_seq, d_m2, k_in, k_out, v_a, v_b;
             d_m2.alloc(d_mem.bytes);
-            FEA_CK(cudaMemcpyAsync(d_seq.p, seq.data(), seq.size() * 4, cudaMemcpyHostToDevice, s));
+            k_in.alloc(n_patch * 4);
+            k_out.alloc(n_patch * 4);
+            v_a.alloc(n_patch * 4);
+            v_b.alloc(n_patch * 4);
+            k_iota32<<<grid_for(n_patch, 256), 256, 0, s>>>(v_a.as<int32_t>(), n_patch);
+            const uint64_t span[3] = {static_cast<uint64_t>(T) * T, static_cast<uint64_t>(nz), static_cast<uint64_t>(tiles)};
+            DevBuf* src = &v_a;
+            DevBuf* dst = &v_b;
+            for (int part = 0; part < 3; ++part) {
+                k_tile_key<<<grid_for(n_patch, 256), 256, 0, s>>>(src->as<int32_t>(), n_patch, s1, s2, T, part,
+                                                                 k_in.as<uint32_t>());
+                int bits = 1;
+                while (bits < 32 && (uint64_t{1} << bits) < span[part]) ++bits;
+                radix_sort_pairs(k_in.as<uint32_t>(), k_out.as<uint32_t>(), src->as<int32_t>(), dst->as<int32_t>(), n_patch, 0,
+                                 bits, s);
+                std::swap(src, dst);
+            }
+            FEA_CK(cudaGetLastError());
+            d_seq = std::move(*src);
             k_permute_members<<<grid_for(n_patch * P, 256), 256, 0, s>>>(d_seq.as<int32_t>(), d_mem.as<int32_t>(), n_patch, P,
                                                                         d_m2.as<int32_t>());
             FEA_CK(cudaGetLastError());
@@ -528,6 +571,7 @@ bool star_patches(fea_plan* p, DevBuf& d_mem, int64_t* n_patch_out, cudaStream_t
     } else if (std::getenv("FEA_PATCH_DEBUG")) {
         std::fprintf(stderr, "patch stars: n_patch %lld\n", (long long)n_patch);
     }
+    mark("tile order");
     *n_patch_out = n_patch;
     return true;
 }
