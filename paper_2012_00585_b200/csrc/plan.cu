@@ -1927,12 +1927,10 @@ fea_status fea_plan_greedy_colouring(const fea_plan* p, int32_t* colour_of, int3
             std::fill(used.begin(), used.end(), 0);
             for (int a = 0; a < npe; ++a) {
                 const int32_t v = conn[e * npe + a];
-                for (int64_t k = ptr[v]; k < ptr[v + 1]; ++k) {
+                for (int64_t k = ptr[v]; k < ptr[v + 1] && adj[k] < e; ++k) {  // (ascending: only earlier elements are coloured)
                     const int c = col[adj[k]];
-                    if (c >= 0) {
-                        if (static_cast<size_t>(c) >= used.size()) used.resize(c + 1, 0);
-                        used[c] = 1;
-                    }
+                    if (static_cast<size_t>(c) >= used.size()) used.resize(c + 1, 0);
+                    used[c] = 1;
                 }
             }
             int c = 0;
