@@ -14,7 +14,7 @@ python tools/bench_configs.py --configs 1,2,3,4 --runs 5 > $OUT/configs.jsonl 2>
 python tools/bench_configs.py --configs 1,2,3 --runs 5 --oracle > $OUT/configs_oracle.jsonl 2> $OUT/configs_oracle.err
 for c in 2 3 5; do python tools/plan_trace.py --config $c --reps 1 --lazy 2> $OUT/lazy_$c.log; done
 python tools/bench_spmv.py --configs 1,2,3,4 > $OUT/spmv.jsonl 2> $OUT/spmv.err
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 2500 --csv \
     --log-file $OUT/launches_bench.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e \
     > $OUT/ncu_bench.log 2>&1
 echo round done
