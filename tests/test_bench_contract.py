@@ -49,6 +49,8 @@ def test_gpu_arm_contract(gpu):
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["e2e"]["values_equal_device_run"] is True
     assert d["clocks"]["sm_mhz"] is not None
+    c = d["config"]
+    assert c["soak_s"] == 0.0 and 0 < c["symbolic_phase_device_dofs_ms_rank0"] and 0 < c["symbolic_phase_ms_rank0"]
 
 
 @pytest.mark.gpu
